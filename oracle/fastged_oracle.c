@@ -1,0 +1,338 @@
+/*
+ * fastged_oracle.c -- CPU ORACLE for the FAST-GED K-Best search (arXiv 2605.00830).
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the plain, slow, obviously-correct
+ * statement of what the CUDA hot path must compute.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+ * load it.  It shares no code, header, table or helper with
+ * paper_2605_00830_b200/ (the product), and the product never calls it.
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md, S:<line> = SPEC.md, and the
+ * readings C1..C27 of SURVEY.md §8(c) O.2 (restated in DESIGN.md §3).
+ *
+ *   Graph  G = (V, E, alpha, beta), simple undirected labelled  (C17)
+ *   Vertex-centric edit operations: substitution, deletion, insertion
+ *   Implied edge operations, three cases
+ *   Cost function: six integer constants, 0 for equal labels      (C1, C2)
+ *   Algorithm 1: level loop, branch, evaluate, keep best K
+ *   Branching: |R_V2| substitutions + one deletion child           (C5)
+ *   Evaluation: PED = E(parent) + c(v<-u) + Imp_cost               (Alg. 2)
+ *   Insertions only after the last level                          (C6)
+ *   best_path <- lambda of the best node in the final List         (C10)
+ *
+ * Readings: g1 vertices are branched in index order v_0..v_{n1-1} (C4);
+ * the deletion child has index j = n2 (C5); every successor of a level competes
+ * in one pool (C27) and exactly min(K, |pool|) are kept, the smallest under the
+ * lexicographic key (PED, p, j) where p is the parent's position in the
+ * canonical frontier order (C12); survivors form the next frontier in ascending
+ * (p, j) order (C13); at the last level the K survivors (selected by PED, C10)
+ * get the completion cost and the argmin by (total, position) is returned.
+ *
+ * Parity pins: see tests/test_oracle_pins.py (worked examples S:64-76,
+ * S:191-213, closed forms, brute force over all partial injections).
+ *
+ * Arithmetic is int64 throughout; nothing is rounded.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+    int32_t n, m;
+    const int32_t *vlabels; /* [n] */
+    const int32_t *edges;   /* [2m] (u, v) pairs */
+    const int32_t *elabels; /* [m] or NULL = every edge has label 0 */
+} og_graph;
+
+typedef struct {
+    int32_t vsub, vdel, vins, esub, edel, eins;
+} og_costs;
+
+/* Per-level record (optional output): frontier size entering the level,
+ * candidates generated, PED of the last kept candidate (-1 when all kept). */
+typedef struct {
+    int64_t frontier;
+    int64_t candidates;
+    int64_t threshold;
+} og_level;
+
+enum { OG_OK = 0, OG_ERR_ARG = 1, OG_ERR_INPUT = 2, OG_ERR_MEM = 3, OG_ERR_SELFCHECK = 7 };
+
+#define DEL (-1)
+
+/* ---- validation: simple undirected graph, no loops, endpoints in range (C17) ---- */
+static int validate_graph(const og_graph *g) {
+    if (!g || g->n < 0 || g->m < 0) return OG_ERR_ARG;
+    if (g->n > 0 && !g->vlabels) return OG_ERR_ARG;
+    if (g->m > 0 && !g->edges) return OG_ERR_ARG;
+    for (int e = 0; e < g->m; e++) {
+        int a = g->edges[2 * e], b = g->edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= g->n || b >= g->n || a == b) return OG_ERR_INPUT;
+    }
+    return OG_OK;
+}
+
+/* Dense adjacency: has[i*n+j] = 1 if edge, lab[i*n+j] = its label.
+ * Returns OG_ERR_INPUT on a duplicate edge (at most one edge per pair). */
+static int dense_adjacency(const og_graph *g, char *has, int32_t *lab) {
+    int n = g->n;
+    memset(has, 0, (size_t)n * n);
+    for (int e = 0; e < g->m; e++) {
+        int a = g->edges[2 * e], b = g->edges[2 * e + 1];
+        int32_t l = g->elabels ? g->elabels[e] : 0;
+        if (has[a * n + b]) return OG_ERR_INPUT;
+        has[a * n + b] = has[b * n + a] = 1;
+        lab[a * n + b] = lab[b * n + a] = l;
+    }
+    return OG_OK;
+}
+
+/* Vertex operation cost: substitution is 0 on equal labels else vsub; deletion vdel. */
+static int64_t vertex_cost(const og_graph *g1, const og_graph *g2, const og_costs *c, int i, int j) {
+    if (j == DEL) return c->vdel;
+    return g1->vlabels[i] == g2->vlabels[j] ? 0 : c->vsub;
+}
+
+/* Implied edge charge between the new operation v_i -> j and an earlier operation
+ * v_q -> t.  Edge in both graphs: substituted, esub unless
+ * labels are equal (C2).  Only in g1: deleted (edel).  Only in g2: inserted (eins).
+ * A deleted endpoint has no g2 image, so its g1 edges are deleted. */
+static int64_t edge_charge(const char *has1, const int32_t *lab1, int n1,
+                           const char *has2, const int32_t *lab2, int n2,
+                           const og_costs *c, int i, int j, int q, int t) {
+    int e1 = has1[i * n1 + q];
+    int e2 = (j != DEL && t != DEL) ? has2[j * n2 + t] : 0;
+    if (e1 && e2) return lab1[i * n1 + q] == lab2[j * n2 + t] ? 0 : c->esub;
+    if (e1) return c->edel;
+    if (e2) return c->eins;
+    return 0;
+}
+
+typedef struct {
+    int64_t ped;
+    int64_t p; /* parent position in the frontier */
+    int32_t j; /* g2 vertex index, or n2 for deletion */
+} cand;
+
+static int cmp_key(const void *x, const void *y) { /* (PED, p, j) ascending (C12) */
+    const cand *a = (const cand *)x, *b = (const cand *)y;
+    if (a->ped != b->ped) return a->ped < b->ped ? -1 : 1;
+    if (a->p != b->p) return a->p < b->p ? -1 : 1;
+    return (a->j > b->j) - (a->j < b->j);
+}
+static int cmp_pos(const void *x, const void *y) { /* (p, j) ascending (C13) */
+    const cand *a = (const cand *)x, *b = (const cand *)y;
+    if (a->p != b->p) return a->p < b->p ? -1 : 1;
+    return (a->j > b->j) - (a->j < b->j);
+}
+
+/* Completion (C6): insert every unused g2 vertex (vins each) and
+ * every g2 edge with at least one unused endpoint (eins each, second-endpoint rule C7). */
+static int64_t completion_cost(const og_graph *g2, const og_costs *c, const char *used) {
+    int64_t s = 0;
+    for (int u = 0; u < g2->n; u++)
+        if (!used[u]) s += c->vins;
+    for (int e = 0; e < g2->m; e++) {
+        int x = g2->edges[2 * e], y = g2->edges[2 * e + 1];
+        if (!used[x] || !used[y]) s += c->eins;
+    }
+    return s;
+}
+
+/* Order-free cost of a complete vertex mapping f: V1 -> V2 u {DEL} (
+ * SURVEY §8(c) O.4).  Used only to re-verify the returned witness. */
+static int64_t mapping_cost(const og_graph *g1, const og_graph *g2, const og_costs *c,
+                            const char *has1, const char *has2, const int32_t *lab2, const int32_t *f) {
+    int n1 = g1->n, n2 = g2->n;
+    int64_t s = 0;
+    char *img = (char *)calloc((size_t)(n2 > 0 ? n2 : 1), 1);
+    int32_t *inv = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n2 > 0 ? n2 : 1));
+    for (int u = 0; u < n2; u++) inv[u] = -1;
+    for (int i = 0; i < n1; i++) {
+        if (f[i] == DEL) s += c->vdel;
+        else {
+            s += (g1->vlabels[i] == g2->vlabels[f[i]]) ? 0 : c->vsub;
+            img[f[i]] = 1;
+            inv[f[i]] = i;
+        }
+    }
+    for (int u = 0; u < n2; u++)
+        if (!img[u]) s += c->vins;
+    for (int e = 0; e < g1->m; e++) {
+        int a = g1->edges[2 * e], b = g1->edges[2 * e + 1];
+        int32_t l1 = g1->elabels ? g1->elabels[e] : 0;
+        if (f[a] != DEL && f[b] != DEL && has2[f[a] * n2 + f[b]])
+            s += (l1 == lab2[f[a] * n2 + f[b]]) ? 0 : c->esub;
+        else
+            s += c->edel;
+    }
+    for (int e = 0; e < g2->m; e++) {
+        int x = g2->edges[2 * e], y = g2->edges[2 * e + 1];
+        int matched = 0;
+        if (img[x] && img[y]) matched = has1[inv[x] * n1 + inv[y]];
+        if (!matched) s += c->eins;
+    }
+    free(img);
+    free(inv);
+    return s;
+}
+
+/*
+ * og_kbest: Algorithm 1 with the readings listed at the top.
+ *   cost_out      : GED upper bound (the cost of the returned edit path)
+ *   mapping_out   : [g1->n] g2 index or -1 (deleted); insertions are implied
+ *   children_out  : total candidates generated over all levels (sum c_i), may be NULL
+ *   parents_out   : total frontier nodes expanded (sum N_i), may be NULL
+ *   levels_out    : [g1->n] per-level record, may be NULL
+ */
+int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t K,
+             int64_t *cost_out, int32_t *mapping_out, int64_t *children_out,
+             int64_t *parents_out, og_level *levels_out) {
+    int rc;
+    if (!c || !cost_out || K < 1) return OG_ERR_ARG;
+    if (c->vsub < 0 || c->vdel < 0 || c->vins < 0 || c->esub < 0 || c->edel < 0 || c->eins < 0)
+        return OG_ERR_ARG;
+    if ((rc = validate_graph(g1)) != OG_OK) return rc;
+    if ((rc = validate_graph(g2)) != OG_OK) return rc;
+    if (g1->n > 0 && !mapping_out) return OG_ERR_ARG;
+
+    const int n1 = g1->n, n2 = g2->n;
+    const size_t a1 = (size_t)(n1 > 0 ? n1 * n1 : 1), a2 = (size_t)(n2 > 0 ? n2 * n2 : 1);
+    char *has1 = (char *)malloc(a1), *has2 = (char *)malloc(a2);
+    int32_t *lab1 = (int32_t *)malloc(a1 * sizeof(int32_t)), *lab2 = (int32_t *)malloc(a2 * sizeof(int32_t));
+    if (dense_adjacency(g1, has1, lab1) != OG_OK || dense_adjacency(g2, has2, lab2) != OG_OK) {
+        free(has1); free(has2); free(lab1); free(lab2);
+        return OG_ERR_INPUT;
+    }
+
+    /* Frontier F_i: node k has ped[k], map[k*n1 + q] for q < i, used[k*n2 + u]. */
+    int64_t N = 1; /* root: lambda empty, all of V2 remaining */
+    int64_t *ped = (int64_t *)calloc(1, sizeof(int64_t));
+    int32_t *map = (int32_t *)calloc((size_t)(n1 > 0 ? n1 : 1), sizeof(int32_t));
+    char *used = (char *)calloc((size_t)(n2 > 0 ? n2 : 1), 1);
+    int64_t children = 0, parents = 0;
+    rc = OG_OK;
+
+    for (int i = 0; i < n1 && rc == OG_OK; i++) { /* ForEach v in V1, order C4 */
+        /* Branch + evaluate every node of List. */
+        int64_t C = N * (int64_t)(n2 + 1);
+        cand *pool = (cand *)malloc(sizeof(cand) * (size_t)C);
+        char *valid = (char *)malloc((size_t)C);
+        if (!pool || !valid) { free(pool); free(valid); rc = OG_ERR_MEM; break; }
+#pragma omp parallel for schedule(dynamic, 64) if (N * (int64_t)(n2 + 1) * (i + 1) > (1 << 20))
+        for (int64_t p = 0; p < N; p++) {
+            for (int j = 0; j <= n2; j++) { /* j = n2 is the deletion child (C5) */
+                int64_t slot = p * (n2 + 1) + j;
+                int op = (j == n2) ? DEL : j;
+                valid[slot] = (op == DEL) || !used[p * n2 + op];
+                if (!valid[slot]) continue;
+                int64_t e = ped[p] + vertex_cost(g1, g2, c, i, op);
+                for (int q = 0; q < i; q++) /* implied edges vs all earlier operations */
+                    e += edge_charge(has1, lab1, n1, has2, lab2, n2, c, i, op, q, map[p * n1 + q]);
+                pool[slot].ped = e;
+                pool[slot].p = p;
+                pool[slot].j = j;
+            }
+        }
+        int64_t cnt = 0;
+        for (int64_t s = 0; s < C; s++)
+            if (valid[s]) pool[cnt++] = pool[s];
+        free(valid);
+        children += cnt;
+        parents += N;
+
+        /* List <- best K nodes of list_tmp: the min(K, cnt) smallest keys (C12). */
+        qsort(pool, (size_t)cnt, sizeof(cand), cmp_key);
+        int64_t keep = cnt < K ? cnt : K;
+        if (levels_out) {
+            levels_out[i].frontier = N;
+            levels_out[i].candidates = cnt;
+            levels_out[i].threshold = (cnt > K) ? pool[keep - 1].ped : -1;
+        }
+        /* Next frontier in canonical (p, j) order (C13). */
+        qsort(pool, (size_t)keep, sizeof(cand), cmp_pos);
+        int64_t *nped = (int64_t *)malloc(sizeof(int64_t) * (size_t)keep);
+        int32_t *nmap = (int32_t *)malloc(sizeof(int32_t) * (size_t)keep * (size_t)n1);
+        char *nused = (char *)malloc((size_t)keep * (size_t)(n2 > 0 ? n2 : 1));
+        if (!nped || !nmap || !nused) { free(pool); free(nped); free(nmap); free(nused); rc = OG_ERR_MEM; break; }
+        for (int64_t k = 0; k < keep; k++) {
+            int64_t p = pool[k].p;
+            int op = pool[k].j == n2 ? DEL : pool[k].j;
+            nped[k] = pool[k].ped;
+            memcpy(nmap + k * n1, map + p * n1, sizeof(int32_t) * (size_t)n1);
+            nmap[k * n1 + i] = op;
+            if (n2 > 0) memcpy(nused + k * n2, used + p * n2, (size_t)n2);
+            if (op != DEL) nused[k * n2 + op] = 1;
+        }
+        free(pool);
+        free(ped); free(map); free(used);
+        ped = nped; map = nmap; used = nused;
+        N = keep;
+    }
+
+    if (rc == OG_OK) {
+        /* Insertions at the end and best_path <- best node (C10). */
+        int64_t best = -1, best_total = 0;
+        for (int64_t k = 0; k < N; k++) {
+            int64_t total = ped[k] + completion_cost(g2, c, used + k * (n2 > 0 ? n2 : 0));
+            if (best < 0 || total < best_total) { best = k; best_total = total; }
+        }
+        for (int q = 0; q < n1; q++) mapping_out[q] = map[best * n1 + q];
+        *cost_out = best_total;
+        if (children_out) *children_out = children;
+        if (parents_out) *parents_out = parents;
+        /* Self-check: the witness re-verifies with the order-free formula. */
+        if (mapping_cost(g1, g2, c, has1, has2, lab2, mapping_out) != best_total) rc = OG_ERR_SELFCHECK;
+    }
+    free(ped); free(map); free(used);
+    free(has1); free(has2); free(lab1); free(lab2);
+    return rc;
+}
+
+/* Independent pairs in parallel (no change to any pair's arithmetic). */
+int og_kbest_batch(int32_t npairs, const og_graph *g1s, const og_graph *g2s, const og_costs *c,
+                   int64_t K, int64_t *costs_out, int32_t *mappings_out, const int64_t *map_offsets,
+                   int64_t *children_out, int32_t nthreads, int32_t *status_out) {
+    if (npairs < 0 || (npairs > 0 && (!g1s || !g2s || !costs_out || !map_offsets || !status_out)))
+        return OG_ERR_ARG;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    int rc = OG_OK;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t k = 0; k < npairs; k++) {
+        int64_t ch = 0;
+        status_out[k] = og_kbest(&g1s[k], &g2s[k], c, K, &costs_out[k],
+                                 mappings_out ? mappings_out + map_offsets[k] : NULL, &ch, NULL, NULL);
+        if (children_out) children_out[k] = ch;
+    }
+    for (int32_t k = 0; k < npairs; k++)
+        if (status_out[k] != OG_OK) { rc = status_out[k]; break; }
+    return rc;
+}
+
+int og_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* Exposed for the witness tests: order-free cost of a given complete mapping. */
+int og_mapping_cost(const og_graph *g1, const og_graph *g2, const og_costs *c, const int32_t *f,
+                    int64_t *cost_out) {
+    int rc;
+    if ((rc = validate_graph(g1)) != OG_OK) return rc;
+    if ((rc = validate_graph(g2)) != OG_OK) return rc;
+    size_t a1 = (size_t)(g1->n > 0 ? g1->n * g1->n : 1), a2 = (size_t)(g2->n > 0 ? g2->n * g2->n : 1);
+    char *has1 = (char *)malloc(a1), *has2 = (char *)malloc(a2);
+    int32_t *lab1 = (int32_t *)malloc(a1 * sizeof(int32_t)), *lab2 = (int32_t *)malloc(a2 * sizeof(int32_t));
+    if (dense_adjacency(g1, has1, lab1) != OG_OK || dense_adjacency(g2, has2, lab2) != OG_OK) rc = OG_ERR_INPUT;
+    else *cost_out = mapping_cost(g1, g2, c, has1, has2, lab2, f);
+    free(has1); free(has2); free(lab1); free(lab2);
+    return rc;
+}
