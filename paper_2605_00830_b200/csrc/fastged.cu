@@ -1,0 +1,880 @@
+// fastged.cu -- host engine and C ABI of the B200 FAST-GED K-Best hot path (include/fastged.h).
+//
+// Host work per call: validate the graphs (reading C17), intern edge labels, pack
+// every pair into one device blob (g2 bit-packed adjacency rows, the P_i lists of earlier g1
+// neighbours, labels), copy it to HBM once ("transferred once"), launch the search
+// kernels, copy results back once.  Nothing of the search runs on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fastged.h"
+#include "batch_kernel.cuh"
+#include "large_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(n, (size_t)4096);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostPinned {
+    void *p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(n, (size_t)4096);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct FgError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw FgError{code, buf};
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            fail(e_ == cudaErrorMemoryAllocation ? FASTGED_ERR_CAPACITY : FASTGED_ERR_CUDA,        \
+                 "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);       \
+    } while (0)
+
+inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+inline int words_for(int n2) { return std::max(1, (n2 + 31) / 32); }
+
+// ---------------------------------------------------------------- packed pair (host side)
+struct PackedPair {
+    fg::PairDesc d;
+    int W;
+    size_t bytes; // blob bytes of this pair
+};
+
+struct GroupKey {
+    int W;
+    bool lab;
+    bool operator<(const GroupKey &o) const { return W != o.W ? W < o.W : lab < o.lab; }
+};
+
+} // namespace
+
+// ---------------------------------------------------------------- handle / batch
+struct fastged_batch {
+    int32_t npairs = 0;
+    std::vector<fg::PairDesc> descs;      // host copy (offsets)
+    std::vector<int> W;                   // per pair
+    std::vector<int64_t> map_off;         // per pair mapping offset
+    int64_t total_map = 0;
+    int n1max = 0, n2max = 0;
+    DevBuf blob, ddesc, dorder, dcost, dmap, dchild, dpar, dalg, dwork;
+    std::map<GroupKey, std::vector<int32_t>> groups; // pair indices per kernel variant
+    std::vector<int32_t> large;                      // pairs beyond the batched limits
+    bool ran = false;
+};
+
+struct fastged_handle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sms = 148;
+    size_t smem_optin = 227 * 1024;
+    uint32_t flags = 0;
+    int world = 1, rank = 0;
+    std::string err;
+    DevBuf scratch, levels;
+    HostPinned stage;
+    fastged_stats_t stats{};
+    std::vector<cudaEvent_t> evpool;
+    int evused = 0;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    DevBuf lblob, lbuf; // large single-pair mode
+};
+
+namespace {
+
+int set_err(fastged_handle_t *h, const FgError &e) {
+    if (h) h->err = e.msg;
+    return e.code;
+}
+
+// ---------------------------------------------------------------- validation
+void validate_graph(const fastged_graph_t *g, int pair, const char *which) {
+    if (!g) fail(FASTGED_ERR_ARG, "pair %d: %s is NULL", pair, which);
+    if (g->n < 0 || g->m < 0) fail(FASTGED_ERR_INPUT, "pair %d: %s has n=%d m=%d", pair, which, g->n, g->m);
+    if (g->n > FASTGED_MAX_N) fail(FASTGED_ERR_CAPACITY, "pair %d: %s has n=%d > %d", pair, which, g->n, FASTGED_MAX_N);
+    if (g->n > 0 && !g->vlabels) fail(FASTGED_ERR_ARG, "pair %d: %s vlabels is NULL", pair, which);
+    if (g->m > 0 && !g->edges) fail(FASTGED_ERR_ARG, "pair %d: %s edges is NULL", pair, which);
+    if ((int64_t)g->m > (int64_t)g->n * (g->n - 1) / 2)
+        fail(FASTGED_ERR_INPUT, "pair %d: %s has more edges than a simple graph allows", pair, which);
+    std::vector<uint64_t> keys((size_t)g->m);
+    for (int e = 0; e < g->m; ++e) {
+        int a = g->edges[2 * e], b = g->edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= g->n || b >= g->n)
+            fail(FASTGED_ERR_INPUT, "pair %d: %s edge %d endpoint out of range", pair, which, e);
+        if (a == b) fail(FASTGED_ERR_INPUT, "pair %d: %s edge %d is a self-loop", pair, which, e);
+        keys[e] = ((uint64_t)std::min(a, b) << 32) | (uint32_t)std::max(a, b);
+    }
+    std::sort(keys.begin(), keys.end());
+    for (size_t e = 1; e < keys.size(); ++e)
+        if (keys[e] == keys[e - 1]) fail(FASTGED_ERR_INPUT, "pair %d: %s has a duplicate edge", pair, which);
+}
+
+void validate_costs(const fastged_costs_t *c) {
+    if (!c) fail(FASTGED_ERR_ARG, "costs is NULL");
+    if (c->vsub < 0 || c->vdel < 0 || c->vins < 0 || c->esub < 0 || c->edel < 0 || c->eins < 0)
+        fail(FASTGED_ERR_ARG, "negative cost");
+}
+
+void check_overflow(const fastged_graph_t *g1, const fastged_graph_t *g2, const fastged_costs_t *c, int pair) {
+    int64_t bound = (int64_t)g1->n * std::max(c->vsub, c->vdel) + (int64_t)g2->n * c->vins +
+                    ((int64_t)g1->m + g2->m) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
+    if (bound >= ((int64_t)1 << 31))
+        fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", pair, (long long)bound);
+}
+
+// Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024, K <= 2^24.
+bool fits_batched(const fastged_graph_t *g1, const fastged_graph_t *g2, int64_t k) {
+    return g2->n <= 128 && g1->n <= 1024 && k <= (1 << 24);
+}
+
+// ---------------------------------------------------------------- packing
+// Sizes a pair's blob segment.
+size_t pair_blob_bytes(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, int n2p) {
+    int W = words_for(g2->n);
+    size_t b = 0;
+    b += align16(4 * (size_t)g1->n);       // vl1
+    b += align16(4 * (size_t)g2->n);       // vl2
+    b += align16(4 * (size_t)(g1->n + 1)); // pptr
+    b += align16(4 * (size_t)g1->m) * 2;   // pq, pl
+    b += align16(4 * (size_t)g2->n * W);   // adj2
+    if (lab) b += align16((size_t)n2p * n2p);
+    return b;
+}
+
+// Edge-label interning: returns true if edge labels can change a cost (more than one distinct label
+// among the edges of both graphs).
+bool labelled_pair(const fastged_graph_t *g1, const fastged_graph_t *g2) {
+    bool have = false;
+    int32_t first = 0;
+    for (const fastged_graph_t *g : {g1, g2})
+        for (int e = 0; e < g->m; ++e) {
+            int32_t l = g->elabels ? g->elabels[e] : 0;
+            if (!have) { have = true; first = l; }
+            else if (l != first) return true;
+        }
+    return false;
+}
+
+void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, int n2p, uint8_t *blob,
+               int64_t off, fg::PairDesc &d, int pair) {
+    const int n1 = g1->n, n2 = g2->n, W = words_for(n2);
+    int64_t cur = off;
+    auto seg = [&](size_t bytes, int64_t &field) {
+        field = cur;
+        uint8_t *q = blob + cur;
+        cur += (int64_t)align16(bytes);
+        return q;
+    };
+    d.n1 = n1; d.n2 = n2; d.m1 = g1->m; d.m2 = g2->m; d.labelled = lab ? 1 : 0; d.n2p = n2p;
+    int32_t *vl1 = (int32_t *)seg(4 * (size_t)n1, d.vl1);
+    int32_t *vl2 = (int32_t *)seg(4 * (size_t)n2, d.vl2);
+    int32_t *pptr = (int32_t *)seg(4 * (size_t)(n1 + 1), d.pptr);
+    int32_t *pq = (int32_t *)seg(4 * (size_t)g1->m, d.pq);
+    int32_t *pl = (int32_t *)seg(4 * (size_t)g1->m, d.pl);
+    uint32_t *adj2 = (uint32_t *)seg(4 * (size_t)n2 * W, d.adj2);
+    uint8_t *e2 = nullptr;
+    if (lab) e2 = seg((size_t)n2p * n2p, d.e2lab);
+    else d.e2lab = 0;
+    if (n1) memcpy(vl1, g1->vlabels, 4 * (size_t)n1);
+    if (n2) memcpy(vl2, g2->vlabels, 4 * (size_t)n2);
+    // g2 label ids: 1..L (0 = no edge); g1 labels absent from g2 -> 255 (never equal)
+    std::map<int32_t, int> ids;
+    if (lab) {
+        for (int e = 0; e < g2->m; ++e) {
+            int32_t l = g2->elabels ? g2->elabels[e] : 0;
+            if (!ids.count(l)) {
+                int id = (int)ids.size() + 1;
+                if (id > FASTGED_MAX_EDGE_LABELS)
+                    fail(FASTGED_ERR_CAPACITY, "pair %d: g2 has more than %d distinct edge labels", pair,
+                         FASTGED_MAX_EDGE_LABELS);
+                ids[l] = id;
+            }
+        }
+        memset(e2, 0, (size_t)n2p * n2p);
+    }
+    // P_i = {q < i : (v_q, v_i) in E1}, each g1 edge listed at its later endpoint (second-endpoint rule, C7)
+    std::vector<int> cnt(n1 + 1, 0);
+    for (int e = 0; e < g1->m; ++e) cnt[std::max(g1->edges[2 * e], g1->edges[2 * e + 1])]++;
+    pptr[0] = 0;
+    for (int i = 0; i < n1; ++i) pptr[i + 1] = pptr[i] + cnt[i];
+    std::vector<int> fillp(pptr, pptr + n1 + 1);
+    for (int e = 0; e < g1->m; ++e) {
+        int a = g1->edges[2 * e], b = g1->edges[2 * e + 1];
+        int q = std::min(a, b), i = std::max(a, b);
+        int at = fillp[i]++;
+        pq[at] = q;
+        int32_t l = g1->elabels ? g1->elabels[e] : 0;
+        if (lab) {
+            auto it = ids.find(l);
+            pl[at] = it == ids.end() ? 255 : it->second;
+        } else pl[at] = 0;
+    }
+    memset(adj2, 0, 4 * (size_t)n2 * W);
+    for (int e = 0; e < g2->m; ++e) {
+        int x = g2->edges[2 * e], y = g2->edges[2 * e + 1];
+        adj2[x * W + (y >> 5)] |= 1u << (y & 31);
+        adj2[y * W + (x >> 5)] |= 1u << (x & 31);
+        if (lab) {
+            int32_t l = g2->elabels ? g2->elabels[e] : 0;
+            uint8_t id = (uint8_t)ids[l];
+            e2[x * n2p + y] = id;
+            e2[y * n2p + x] = id;
+        }
+    }
+}
+
+cudaEvent_t next_event(fastged_handle_t *h) {
+    if (h->evused == (int)h->evpool.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        h->evpool.push_back(e);
+    }
+    return h->evpool[h->evused++];
+}
+
+// ---------------------------------------------------------------- batch build
+fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph_t *g1s,
+                           const fastged_graph_t *g2s) {
+    if (npairs < 0) fail(FASTGED_ERR_ARG, "npairs < 0");
+    if (npairs > 0 && (!g1s || !g2s)) fail(FASTGED_ERR_ARG, "graph arrays are NULL");
+    fastged_batch *b = new fastged_batch();
+    try {
+        b->npairs = npairs;
+        b->descs.resize(npairs);
+        b->W.resize(npairs);
+        b->map_off.resize(npairs + 1);
+        std::vector<char> lab(npairs);
+        std::vector<int> n2p(npairs);
+        std::vector<int64_t> off(npairs + 1);
+        off[0] = 0;
+        b->map_off[0] = 0;
+        for (int p = 0; p < npairs; ++p) {
+            validate_graph(&g1s[p], p, "g1");
+            validate_graph(&g2s[p], p, "g2");
+            lab[p] = labelled_pair(&g1s[p], &g2s[p]);
+            n2p[p] = (g2s[p].n + 3) & ~3;
+            off[p + 1] = off[p] + (int64_t)pair_blob_bytes(&g1s[p], &g2s[p], lab[p], n2p[p]);
+            b->map_off[p + 1] = b->map_off[p] + g1s[p].n;
+            b->n1max = std::max(b->n1max, g1s[p].n);
+            b->n2max = std::max(b->n2max, g2s[p].n);
+        }
+        b->total_map = b->map_off[npairs];
+        size_t blob_bytes = (size_t)off[npairs];
+        size_t desc_bytes = sizeof(fg::PairDesc) * (size_t)std::max(npairs, 1);
+        CK(h->stage.reserve(blob_bytes + desc_bytes + 64));
+        uint8_t *stage = (uint8_t *)h->stage.p;
+        for (int p = 0; p < npairs; ++p) {
+            pack_pair(&g1s[p], &g2s[p], lab[p], n2p[p], stage, off[p], b->descs[p], p);
+            b->descs[p].map_out = b->map_off[p];
+            b->W[p] = words_for(g2s[p].n);
+        }
+        memcpy(stage + blob_bytes, b->descs.data(), sizeof(fg::PairDesc) * (size_t)npairs);
+        CK(b->blob.reserve(blob_bytes + 16));
+        CK(b->ddesc.reserve(desc_bytes));
+        CK(b->dorder.reserve(4 * (size_t)std::max(npairs, 1)));
+        CK(b->dcost.reserve(8 * (size_t)std::max(npairs, 1)));
+        CK(b->dchild.reserve(8 * (size_t)std::max(npairs, 1)));
+        CK(b->dpar.reserve(8 * (size_t)std::max(npairs, 1)));
+        CK(b->dalg.reserve(8 * (size_t)std::max(npairs, 1)));
+        CK(b->dmap.reserve(4 * (size_t)std::max<int64_t>(b->total_map, 1)));
+        CK(b->dwork.reserve(64 * sizeof(int)));
+        if (blob_bytes) CK(cudaMemcpyAsync(b->blob.p, stage, blob_bytes, cudaMemcpyHostToDevice, h->stream));
+        if (npairs) CK(cudaMemcpyAsync(b->ddesc.p, stage + blob_bytes, sizeof(fg::PairDesc) * npairs,
+                                       cudaMemcpyHostToDevice, h->stream));
+        h->stats.h2d_bytes += (int64_t)(blob_bytes + sizeof(fg::PairDesc) * npairs);
+        CK(cudaStreamSynchronize(h->stream)); // staging buffer is reused by the next call
+        return b;
+    } catch (...) {
+        b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
+        b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
+        delete b;
+        throw;
+    }
+}
+
+template <int W, bool LAB>
+void launch_group(fastged_handle_t *h, fastged_batch *b, const fg::BatchArgs &args, int grid, size_t smem) {
+    auto kern = fg::kbest_batch_kernel<W, LAB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 256, smem, h->stream>>>(args);
+    CK(cudaGetLastError());
+}
+
+void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, int64_t k,
+               int64_t *levels_dev) {
+    validate_costs(c);
+    if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
+    // group pairs by kernel variant; schedule the largest pairs first (dynamic counter)
+    b->groups.clear();
+    b->large.clear();
+    // host copies of the graphs are gone after upload; the descriptors hold the sizes
+    for (int p = 0; p < b->npairs; ++p) {
+        const fg::PairDesc &d = b->descs[p];
+        int64_t bound = (int64_t)d.n1 * std::max(c->vsub, c->vdel) + (int64_t)d.n2 * c->vins +
+                        ((int64_t)d.m1 + d.m2) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
+        if (bound >= ((int64_t)1 << 31))
+            fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", p, (long long)bound);
+        if (d.n2 <= 128 && d.n1 <= 1024 && k <= (1 << 24))
+            b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
+        else
+            b->large.push_back(p);
+    }
+    if (!b->large.empty())
+        fail(FASTGED_ERR_CAPACITY, "pair %d exceeds the batched limits (n2 <= 128, n1 <= 1024, k <= 2^24); "
+                                   "solve it with fastged_solve_pair", b->large[0]);
+    h->evused = 0;
+    h->stats.kernel_launches = 0;
+    h->stats.branch_launches = 0;
+    h->stats.branch_ms = 0.f;
+    std::vector<int32_t> order_all;
+    std::vector<std::pair<GroupKey, std::pair<size_t, size_t>>> spans;
+    for (auto &kv : b->groups) {
+        auto &v = kv.second;
+        std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
+            const fg::PairDesc &a = b->descs[x], &bb = b->descs[y];
+            return (int64_t)a.n1 * (a.n2 + 1) > (int64_t)bb.n1 * (bb.n2 + 1);
+        });
+        spans.push_back({kv.first, {order_all.size(), v.size()}});
+        order_all.insert(order_all.end(), v.begin(), v.end());
+    }
+    CK(h->stage.reserve(4 * order_all.size() + 64));
+    if (!order_all.empty()) {
+        memcpy(h->stage.p, order_all.data(), 4 * order_all.size());
+        CK(cudaMemcpyAsync(b->dorder.p, h->stage.p, 4 * order_all.size(), cudaMemcpyHostToDevice, h->stream));
+        h->stats.h2d_bytes += (int64_t)(4 * order_all.size());
+    }
+    CK(cudaMemsetAsync(b->dwork.p, 0, 64 * sizeof(int), h->stream));
+    CK(cudaEventRecord(h->ev_begin, h->stream));
+    int gi = 0;
+    for (auto &sp : spans) {
+        const GroupKey key = sp.first;
+        const size_t start = sp.second.first, cnt = sp.second.second;
+        int n1max = 0, n2max = 0;
+        for (size_t x = start; x < start + cnt; ++x) {
+            n1max = std::max(n1max, b->descs[order_all[x]].n1);
+            n2max = std::max(n2max, b->descs[order_all[x]].n2);
+        }
+        const int W = key.W;
+        const int K = (int)k;
+        fg::BatchArgs a{};
+        a.descs = (const fg::PairDesc *)b->ddesc.p;
+        a.order = (const int32_t *)b->dorder.p + start;
+        a.ngroup = (int)cnt;
+        a.blob = (const uint8_t *)b->blob.p;
+        a.work = (int32_t *)b->dwork.p + gi;
+        a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
+        a.K = K;
+        a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
+        a.n1s = std::max(4, (n1max + 3) & ~3);
+        a.n1max = std::max(1, n1max);
+        a.csmax = (n2max + 1 + 3) & ~3;
+        int n2p = (n2max + 3) & ~3;
+        a.e2bytes = key.lab ? (int)align16((size_t)n2p * n2p) : 0;
+        size_t codes_bytes = align16((size_t)K * a.csmax), sel_bytes = align16(4 * (size_t)K);
+        size_t smem = align16(8 * (size_t)a.n1max) + a.e2bytes;
+        a.codes_in_smem = (smem + codes_bytes <= 96 * 1024) ? 1 : 0;
+        if (a.codes_in_smem) smem += codes_bytes;
+        a.sel_in_smem = (smem + sel_bytes <= 112 * 1024) ? 1 : 0;
+        if (a.sel_in_smem) smem += sel_bytes;
+        if (smem > h->smem_optin - 4096) fail(FASTGED_ERR_CAPACITY, "shared memory plan too large");
+        // fix e2 carve: P list is 2 * n1max int32
+        size_t per_cta = 2 * 4 * (size_t)K + 2 * 4 * (size_t)K * W + 2 * (size_t)K * a.n1s;
+        if (!a.codes_in_smem) per_cta += codes_bytes;
+        if (!a.sel_in_smem) per_cta += sel_bytes;
+        per_cta = (per_cta + 255) & ~(size_t)255;
+        int occ = 0;
+        cudaError_t oe;
+        switch (W * 2 + (key.lab ? 1 : 0)) {
+#define OCC(WW, LL)                                                                                            \
+    case WW * 2 + LL:                                                                                          \
+        CK(cudaFuncSetAttribute(fg::kbest_batch_kernel<WW, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                (int)smem));                                                                   \
+        oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fg::kbest_batch_kernel<WW, LL>, 256, smem);    \
+        break;
+            OCC(1, 0) OCC(1, 1) OCC(2, 0) OCC(2, 1) OCC(3, 0) OCC(3, 1) OCC(4, 0) OCC(4, 1)
+#undef OCC
+        default: fail(FASTGED_ERR_ARG, "bad variant");
+        }
+        CK(oe);
+        occ = std::max(occ, 1);
+        int grid = (int)std::min<int64_t>((int64_t)cnt, (int64_t)occ * h->sms);
+        // bound scratch to the device: shrink the grid, never K
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        size_t need = per_cta * (size_t)grid;
+        if (need > h->scratch.cap) {
+            size_t avail = free_b + h->scratch.cap;
+            if (per_cta > avail / 2) fail(FASTGED_ERR_CAPACITY, "frontier scratch %zu B per CTA exceeds device memory", per_cta);
+            while (grid > 1 && per_cta * (size_t)grid > avail * 3 / 4) grid--;
+            h->scratch.release();
+            CK(h->scratch.reserve(per_cta * (size_t)grid));
+        }
+        a.scratch = (uint8_t *)h->scratch.p;
+        a.scratch_stride = (int64_t)per_cta;
+        a.cost_out = (int64_t *)b->dcost.p;
+        a.map_out = (int32_t *)b->dmap.p;
+        a.children_out = (int64_t *)b->dchild.p;
+        a.parents_out = (int64_t *)b->dpar.p;
+        a.algbytes_out = (int64_t *)b->dalg.p;
+        a.levels_out = levels_dev;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (h->flags & FASTGED_FLAG_TIMING) {
+            e0 = next_event(h);
+            e1 = next_event(h);
+            CK(cudaEventRecord(e0, h->stream));
+        }
+        switch (W * 2 + (key.lab ? 1 : 0)) {
+        case 2: launch_group<1, false>(h, b, a, grid, smem); break;
+        case 3: launch_group<1, true>(h, b, a, grid, smem); break;
+        case 4: launch_group<2, false>(h, b, a, grid, smem); break;
+        case 5: launch_group<2, true>(h, b, a, grid, smem); break;
+        case 6: launch_group<3, false>(h, b, a, grid, smem); break;
+        case 7: launch_group<3, true>(h, b, a, grid, smem); break;
+        case 8: launch_group<4, false>(h, b, a, grid, smem); break;
+        case 9: launch_group<4, true>(h, b, a, grid, smem); break;
+        default: fail(FASTGED_ERR_ARG, "bad variant");
+        }
+        if (e1) CK(cudaEventRecord(e1, h->stream));
+        h->stats.kernel_launches++;
+        gi++;
+    }
+    CK(cudaEventRecord(h->ev_end, h->stream));
+    b->ran = true;
+}
+
+void finish_timing(fastged_handle_t *h) {
+    float ms = 0.f;
+    CK(cudaEventSynchronize(h->ev_end));
+    CK(cudaEventElapsedTime(&ms, h->ev_begin, h->ev_end));
+    h->stats.device_ms = ms;
+    if (h->flags & FASTGED_FLAG_TIMING) {
+        float tot = 0.f;
+        for (int x = 0; x + 1 < h->evused; x += 2) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, h->evpool[x], h->evpool[x + 1]));
+            tot += t;
+        }
+        h->stats.branch_ms = tot;
+        h->stats.branch_launches = h->evused / 2;
+    }
+}
+
+void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t *mappings_out,
+              int64_t *children_out) {
+    if (!b->ran) fail(FASTGED_ERR_ARG, "batch was not run");
+    if (b->npairs > 0 && !costs_out) fail(FASTGED_ERR_ARG, "costs_out is NULL");
+    if (b->total_map > 0 && !mappings_out) fail(FASTGED_ERR_ARG, "mappings_out is NULL");
+    const size_t P = (size_t)b->npairs, M = (size_t)b->total_map;
+    CK(h->stage.reserve(8 * P * 4 + 4 * M + 64));
+    uint8_t *st = (uint8_t *)h->stage.p;
+    int64_t *hc = (int64_t *)st, *hch = hc + P, *hpa = hch + P, *hal = hpa + P;
+    int32_t *hm = (int32_t *)(hal + P);
+    if (P) {
+        CK(cudaMemcpyAsync(hc, b->dcost.p, 8 * P, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(hch, b->dchild.p, 8 * P, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(hpa, b->dpar.p, 8 * P, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(hal, b->dalg.p, 8 * P, cudaMemcpyDeviceToHost, h->stream));
+    }
+    if (M) CK(cudaMemcpyAsync(hm, b->dmap.p, 4 * M, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    finish_timing(h);
+    h->stats.d2h_bytes += (int64_t)(32 * P + 4 * M);
+    if (P) memcpy(costs_out, hc, 8 * P);
+    if (M) memcpy(mappings_out, hm, 4 * M);
+    if (children_out && P) memcpy(children_out, hch, 8 * P);
+    int64_t ch = 0, pa = 0, al = 0;
+    for (size_t p = 0; p < P; ++p) { ch += hch[p]; pa += hpa[p]; al += hal[p]; }
+    h->stats.children_evaluated = ch;
+    h->stats.parents_expanded = pa;
+    h->stats.alg_bytes = al;
+}
+
+void free_batch(fastged_batch *b) {
+    if (!b) return;
+    b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
+    b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
+    delete b;
+}
+
+void begin_call(fastged_handle_t *h) {
+    h->err.clear();
+    h->stats = fastged_stats_t{};
+    CK(cudaSetDevice(h->device));
+}
+
+
+// Largest frontier any level can hold: N_{i+1} <= min(K, N_i (n2 + 1)), N_0 = 1.
+int64_t frontier_cap(int n1, int n2, int64_t k) {
+    int64_t N = 1, mx = 1;
+    for (int i = 0; i < n1 && N < k; ++i) {
+        N = std::min<int64_t>(k, N * (int64_t)(n2 + 1));
+        mx = std::max(mx, N);
+    }
+    return std::min(mx, k);
+}
+
+void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
+                 const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out) {
+    const int n1 = g1->n, n2 = g2->n;
+    if (n2 > FASTGED_MAX_N2) fail(FASTGED_ERR_CAPACITY, "target graph has n2=%d > %d (limit of this build)", n2, FASTGED_MAX_N2);
+    const int64_t Kc64 = frontier_cap(n1, n2, k);
+    if (Kc64 > (int64_t)1 << 30) fail(FASTGED_ERR_CAPACITY, "frontier cap %lld too large", (long long)Kc64);
+    const int Kc = (int)Kc64;
+    const bool lab = labelled_pair(g1, g2);
+    const int n2p = (n2 + 3) & ~3;
+    const size_t blob_bytes = pair_blob_bytes(g1, g2, lab, n2p);
+    CK(h->stage.reserve(blob_bytes + 64));
+    fg::PairDesc pd{};
+    pack_pair(g1, g2, lab, n2p, (uint8_t *)h->stage.p, 0, pd, 0);
+    pd.map_out = 0;
+    CK(h->lblob.reserve(blob_bytes + 16));
+    CK(cudaMemcpyAsync(h->lblob.p, h->stage.p, blob_bytes, cudaMemcpyHostToDevice, h->stream));
+    h->stats.h2d_bytes += (int64_t)blob_bytes;
+
+    const int W = words_for(n2), Wp = std::max(32, (n2 + 31) & ~31);
+    const bool wide = n2 > 254;
+    const int esz = wide ? 2 : 1;
+    const int n1s = wide ? std::max(2, (n1 + 1) & ~1) : std::max(4, (n1 + 3) & ~3);
+    const int cs = (n2 + 1 + 3) & ~3;
+    size_t smem_masks = 8 * 3 * (size_t)W * 4;
+    size_t smem_adj = (size_t)W * Wp * 4;
+    int adj_in_smem = (smem_masks + smem_adj <= 160 * 1024) ? 1 : 0;
+    size_t smem = smem_masks + (adj_in_smem ? smem_adj : 0);
+    // occupancy -> cooperative grid
+    int occ = 0;
+    void *kfn = nullptr;
+    if (wide) kfn = lab ? (void *)fg::kbest_large_kernel<uint16_t, true> : (void *)fg::kbest_large_kernel<uint16_t, false>;
+    else kfn = lab ? (void *)fg::kbest_large_kernel<uint8_t, true> : (void *)fg::kbest_large_kernel<uint8_t, false>;
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, smem));
+    if (occ < 1) fail(FASTGED_ERR_CAPACITY, "large-mode kernel does not fit on an SM (smem %zu)", smem);
+    occ = std::min(occ, 4);
+    const int grid = occ * h->sms;
+    const int GW = grid * 8;
+    // device buffers
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+    size_t o_ped0 = take(4 * (size_t)Kc), o_ped1 = take(4 * (size_t)Kc);
+    size_t o_used0 = take(4 * (size_t)Kc * W), o_used1 = take(4 * (size_t)Kc * W);
+    size_t o_map0 = take((size_t)esz * n1s * Kc), o_map1 = take((size_t)esz * n1s * Kc);
+    size_t o_codes = take((size_t)Kc * cs), o_selp = take(4 * (size_t)Kc), o_selj = take(4 * (size_t)Kc);
+    size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1)), o_lo = take(4 * (size_t)(n1 + 2));
+    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(24);
+    size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
+    CK(h->lbuf.reserve(off));
+    uint8_t *B = (uint8_t *)h->lbuf.p;
+    CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
+    CK(cudaMemsetAsync(B + o_ci, 0, 8 * (size_t)(n1 + 1), h->stream));
+    CK(cudaMemsetAsync(B + o_lo, 0x7f, 4 * (size_t)(n1 + 2), h->stream));
+    CK(cudaMemsetAsync(B + o_best, 0xff, 8, h->stream));
+    fg::LargeArgs a{};
+    a.blob = (const uint8_t *)h->lblob.p;
+    a.pd = pd;
+    a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
+    a.K = Kc;
+    a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
+    a.W = W;
+    a.Wp = Wp;
+    a.n1s = n1s;
+    a.adj_in_smem = adj_in_smem;
+    a.ped[0] = (int32_t *)(B + o_ped0); a.ped[1] = (int32_t *)(B + o_ped1);
+    a.used[0] = (uint32_t *)(B + o_used0); a.used[1] = (uint32_t *)(B + o_used1);
+    a.map[0] = B + o_map0; a.map[1] = B + o_map1;
+    a.codes = B + o_codes;
+    a.sel_p = (int32_t *)(B + o_selp); a.sel_j = (int32_t *)(B + o_selj);
+    a.hist = (int32_t *)(B + o_hist);
+    a.ci = (int64_t *)(B + o_ci);
+    a.lo = (int32_t *)(B + o_lo);
+    a.wlt = (int32_t *)(B + o_wlt); a.weq = (int32_t *)(B + o_weq);
+    a.best = (unsigned long long *)(B + o_best);
+    a.out = (int64_t *)(B + o_out);
+    a.map_out = (int32_t *)(B + o_mapout);
+    a.levels_out = levels_out ? (int64_t *)(B + o_lev) : nullptr;
+    h->evused = 0;
+    cudaEvent_t e0 = next_event(h), e1 = next_event(h);
+    CK(cudaEventRecord(h->ev_begin, h->stream));
+    CK(cudaEventRecord(e0, h->stream));
+    void *params[] = {(void *)&a};
+    CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(256), params, smem, h->stream));
+    CK(cudaEventRecord(e1, h->stream));
+    CK(cudaEventRecord(h->ev_end, h->stream));
+    h->stats.kernel_launches = 1;
+    int64_t res[4];
+    CK(cudaMemcpyAsync(res, a.out, 32, cudaMemcpyDeviceToHost, h->stream));
+    if (n1) CK(cudaMemcpyAsync(out->mapping, a.map_out, 4 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
+    if (levels_out && n1) CK(cudaMemcpyAsync(levels_out, a.levels_out, 24 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0.f, kms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev_begin, h->ev_end));
+    CK(cudaEventElapsedTime(&kms, e0, e1));
+    h->stats.device_ms = ms;
+    h->stats.branch_ms = kms;
+    h->stats.branch_launches = 1;
+    h->stats.children_evaluated = res[1];
+    h->stats.parents_expanded = res[2];
+    h->stats.alg_bytes = res[3];
+    h->stats.d2h_bytes += 32 + 4 * (int64_t)n1;
+    out->cost = res[0];
+    out->children_evaluated = res[1];
+    out->parents_expanded = res[2];
+    out->device_ms = ms;
+}
+
+} // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char *fastged_version(void) { return "fastged-b200 0.1 sm_100a"; }
+
+int fastged_create(const fastged_config_t *cfg, fastged_handle_t **out) {
+    g_create_error.clear();
+    if (!out) { g_create_error = "out is NULL"; return FASTGED_ERR_ARG; }
+    *out = nullptr;
+    fastged_handle_t *h = nullptr;
+    try {
+        if (!cfg) fail(FASTGED_ERR_ARG, "cfg is NULL");
+        if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+            fail(FASTGED_ERR_ARG, "bad world_size/rank");
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0)
+            fail(FASTGED_ERR_CUDA, "no CUDA device available (%s); this library has no CPU path",
+                 e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+        if (cfg->device < 0 || cfg->device >= ndev) fail(FASTGED_ERR_ARG, "device %d out of range", cfg->device);
+        h = new fastged_handle_t();
+        h->device = cfg->device;
+        h->flags = cfg->flags;
+        h->world = cfg->world_size;
+        h->rank = cfg->rank;
+        CK(cudaSetDevice(h->device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, h->device));
+        if (prop.major < 10) fail(FASTGED_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", h->device, prop.major, prop.minor);
+        h->sms = prop.multiProcessorCount;
+        h->smem_optin = prop.sharedMemPerBlockOptin;
+        if (cfg->stream) h->stream = (cudaStream_t)cfg->stream;
+        else {
+            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        }
+        CK(cudaEventCreate(&h->ev_begin));
+        CK(cudaEventCreate(&h->ev_end));
+        if (h->world > 1)
+            fail(FASTGED_ERR_ARG, "world_size > 1 (sharded single-pair mode) is not available in this build");
+        *out = h;
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        g_create_error = e.msg;
+        if (h) fastged_destroy(h);
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_create_error = "host allocation failed";
+        if (h) fastged_destroy(h);
+        return FASTGED_ERR_CAPACITY;
+    }
+}
+
+void fastged_destroy(fastged_handle_t *h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    h->lblob.release();
+    h->lbuf.release();
+    h->scratch.release();
+    h->levels.release();
+    h->stage.release();
+    for (auto e : h->evpool) cudaEventDestroy(e);
+    if (h->ev_begin) cudaEventDestroy(h->ev_begin);
+    if (h->ev_end) cudaEventDestroy(h->ev_end);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+const char *fastged_last_error(const fastged_handle_t *h) {
+    return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int fastged_get_stats(const fastged_handle_t *h, fastged_stats_t *out) {
+    if (!h || !out) return FASTGED_ERR_ARG;
+    *out = h->stats;
+    return FASTGED_OK;
+}
+
+int fastged_batch_upload(fastged_handle_t *h, int32_t npairs, const fastged_graph_t *g1s,
+                         const fastged_graph_t *g2s, fastged_batch_t **out) {
+    if (!h) return FASTGED_ERR_ARG;
+    try {
+        if (!out) fail(FASTGED_ERR_ARG, "out is NULL");
+        *out = nullptr;
+        begin_call(h);
+        *out = build_batch(h, npairs, g1s, g2s);
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        return set_err(h, e);
+    } catch (const std::bad_alloc &) {
+        return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
+    }
+}
+
+int fastged_batch_run(fastged_handle_t *h, fastged_batch_t *b, const fastged_costs_t *c, int64_t k) {
+    if (!h) return FASTGED_ERR_ARG;
+    try {
+        if (!b) fail(FASTGED_ERR_ARG, "batch is NULL");
+        begin_call(h);
+        run_batch(h, b, c, k, nullptr);
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        return set_err(h, e);
+    } catch (const std::bad_alloc &) {
+        return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
+    }
+}
+
+int fastged_batch_download(fastged_handle_t *h, fastged_batch_t *b, int64_t *costs_out, int32_t *mappings_out,
+                           int64_t *children_out) {
+    if (!h) return FASTGED_ERR_ARG;
+    try {
+        if (!b) fail(FASTGED_ERR_ARG, "batch is NULL");
+        CK(cudaSetDevice(h->device));
+        download(h, b, costs_out, mappings_out, children_out);
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        return set_err(h, e);
+    }
+}
+
+void fastged_batch_free(fastged_handle_t *h, fastged_batch_t *b) {
+    if (h) {
+        cudaSetDevice(h->device);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+    }
+    free_batch(b);
+}
+
+int fastged_solve_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph_t *g1s,
+                        const fastged_graph_t *g2s, const fastged_costs_t *c, int64_t k, int64_t *costs_out,
+                        int32_t *mappings_out, int64_t *children_out) {
+    if (!h) return FASTGED_ERR_ARG;
+    fastged_batch *b = nullptr;
+    try {
+        begin_call(h);
+        validate_costs(c);
+        if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
+        b = build_batch(h, npairs, g1s, g2s);
+        run_batch(h, b, c, k, nullptr);
+        download(h, b, costs_out, mappings_out, children_out);
+        free_batch(b);
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        return set_err(h, e);
+    } catch (const std::bad_alloc &) {
+        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
+    }
+}
+
+int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
+                          const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out) {
+    if (!h) return FASTGED_ERR_ARG;
+    fastged_batch *b = nullptr;
+    try {
+        begin_call(h);
+        if (!out) fail(FASTGED_ERR_ARG, "out is NULL");
+        validate_costs(c);
+        if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
+        validate_graph(g1, 0, "g1");
+        validate_graph(g2, 0, "g2");
+        check_overflow(g1, g2, c, 0);
+        if (g1->n > 0 && !out->mapping) fail(FASTGED_ERR_ARG, "out->mapping is NULL");
+        if (!fits_batched(g1, g2, k) || (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
+            solve_large(h, g1, g2, c, k, out, levels_out);
+            return FASTGED_OK;
+        }
+        b = build_batch(h, 1, g1, g2);
+        int64_t *lev = nullptr;
+        if (levels_out && g1->n > 0) {
+            CK(h->levels.reserve(24 * (size_t)g1->n));
+            lev = (int64_t *)h->levels.p;
+        }
+        run_batch(h, b, c, k, lev);
+        int64_t cost = 0, ch = 0;
+        download(h, b, &cost, out->mapping, &ch);
+        if (lev) CK(cudaMemcpy(levels_out, lev, 24 * (size_t)g1->n, cudaMemcpyDeviceToHost));
+        out->cost = cost;
+        out->children_evaluated = h->stats.children_evaluated;
+        out->parents_expanded = h->stats.parents_expanded;
+        out->device_ms = h->stats.device_ms;
+        free_batch(b);
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        return set_err(h, e);
+    } catch (const std::bad_alloc &) {
+        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
+    }
+}
+
+int fastged_solve_pair(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
+                       const fastged_costs_t *c, int64_t k, fastged_result_t *out) {
+    return fastged_solve_pair_ex(h, g1, g2, c, k, out, nullptr);
+}
+
+} // extern "C"
