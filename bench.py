@@ -138,7 +138,10 @@ def run_ours(args, rank, local_rank, world):
     build.build()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the library launches on it and the CUDA events time it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     w = workload(rank, args.npairs, args.K)
     packed = binding.PackedGraphs(w.graphs)
     h = binding.Handle(local_rank, stream=stream.cuda_stream, flags=binding.FLAG_TIMING)
@@ -158,7 +161,7 @@ def run_ours(args, rank, local_rank, world):
     clocks = ClockSampler(local_rank)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    branch_ms, branch_launches, launches, alg_bytes, children, parents = 0.0, 0, 0, 0, 0, 0
+    branch_ms, branch_launches, launches, alg_bytes, children, parents, lib_ms = 0.0, 0, 0, 0, 0, 0, 0.0
     barrier()
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()
@@ -170,6 +173,7 @@ def run_ours(args, rank, local_rank, world):
         out = batch.download()  # per-step result read (also fills per-launch kernel timings)
         st = h.stats()
         branch_ms += st["branch_ms"]
+        lib_ms += st["device_ms"]
         branch_launches += st["branch_launches"]
         launches += st["kernel_launches"]
         alg_bytes += st["alg_bytes"]
@@ -180,6 +184,8 @@ def run_ours(args, rank, local_rank, world):
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    # the library's own events (same stream) must agree with ours: guards against timing the wrong stream
+    assert abs(dev_ms - lib_ms) <= 0.05 * max(dev_ms, lib_ms) + 0.05, (dev_ms, lib_ms)
     assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1]), "results changed between steps"
 
     # ---- end-to-end through the public API with host buffers (H2D + search + D2H each step)

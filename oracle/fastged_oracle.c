@@ -57,6 +57,7 @@ typedef struct {
     int64_t frontier;
     int64_t candidates;
     int64_t threshold;
+    int64_t min_ped;    /* smallest candidate PED of the level */
 } og_level;
 
 enum { OG_OK = 0, OG_ERR_ARG = 1, OG_ERR_INPUT = 2, OG_ERR_MEM = 3, OG_ERR_SELFCHECK = 7 };
@@ -251,6 +252,7 @@ int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t 
             levels_out[i].frontier = N;
             levels_out[i].candidates = cnt;
             levels_out[i].threshold = (cnt > K) ? pool[keep - 1].ped : -1;
+            levels_out[i].min_ped = cnt > 0 ? pool[0].ped : -1;
         }
         /* Next frontier in canonical (p, j) order (C13). */
         qsort(pool, (size_t)keep, sizeof(cand), cmp_pos);

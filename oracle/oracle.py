@@ -26,7 +26,8 @@ class OgCosts(C.Structure):
 
 
 class OgLevel(C.Structure):
-    _fields_ = [("frontier", C.c_int64), ("candidates", C.c_int64), ("threshold", C.c_int64)]
+    _fields_ = [("frontier", C.c_int64), ("candidates", C.c_int64), ("threshold", C.c_int64),
+                ("min_ped", C.c_int64)]
 
 
 ERRORS = {0: "ok", 1: "bad argument", 2: "invalid graph", 3: "out of memory", 7: "witness self-check failed"}
@@ -101,6 +102,7 @@ def kbest(g1, g2, costs, K, levels: bool = False):
     out = dict(cost=int(cost.value), mapping=mp[: int(g1.n)].copy(), children=int(ch.value), parents=int(pa.value))
     if levels:
         out["levels"] = [(lv[i].frontier, lv[i].candidates, lv[i].threshold) for i in range(int(g1.n))]
+        out["min_ped"] = [lv[i].min_ped for i in range(int(g1.n))]
     return out
 
 

@@ -15,7 +15,7 @@ DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "larg
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v", "-shared",
+    "-Xcompiler", "-fPIC,-O2,-Wall,-fopenmp", "-Xptxas", "-v", "-shared",
 ]
 
 
@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SRCS, "-lcudart"]
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SRCS, "-lcudart", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "csrc", "ptxas.log")
     with open(log, "w") as f:

@@ -1,7 +1,14 @@
 // batch_kernel.cuh -- the batched K-Best search: one CTA runs one (g1, g2) pair through all
 // levels of Alg. 1 and then takes the next pair from a work counter.
 //
-// Per level i (g1 vertex v_i, reading C4) the CTA runs:
+// Frontier (per CTA, global scratch, structure-of-arrays so every per-level pass is coalesced):
+//   ped[K] int32, usedT[W][K] uint32 (bit u = g2 vertex u used), mapT[n1][K] uint8 (lambda,
+//   255 = deleted).  Column k of usedT/mapT is frontier node k.
+//
+// Per level i (g1 vertex v_i, reading C4):
+//   P  Parent prepass (thread per parent): PED, used mask and B_p -- the images of the earlier
+//      g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors) -- are staged
+//      in shared memory; the lambda gathers are coalesced across parents (transposed layout).
 //   A  Branch (Alg. 2).  A warp takes one parent at a time;
 //      lane l owns the g2 vertices u = l + 32 s (s < W), whose bit-packed adjacency rows stay in
 //      registers for the whole pair.  The child PED is the paper's incremental evaluation
@@ -9,27 +16,28 @@
 //      regrouped into popcounts:
 //          Delta(u)   = cv(i,u) + edel*d_i + eins*cnt_p(u) - (edel+eins)*cB_p(u) + esub*mis_p(u)
 //          Delta(DEL) = vdel + edel*d_i
-//      cnt_p(u) = popc(adj2[u] & used_p), cB_p(u) = popc(adj2[u] & B_p), B_p = images of the
-//      earlier g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors).
-//      Each child is written as a one-byte rank code (PED - base + 1, saturated) and counted in
-//      a shared-memory histogram.  Children never reach HBM.
-//   T  Threshold (PAPER.md:261-265 local/global ranking, replaced): the histogram prefix gives
-//      the threshold PED t and the quota r of ties at t; exactly min(K, c_i) children are kept,
-//      the smallest under (PED, parent, child) (reading C12).  No sort.
-//   B  Per-warp counts of codes < t and == t (SIMD byte compares), then a warp-level prefix gives
-//      each warp its tie admissions and output offset.
-//   C  Update: survivors are compacted in (parent, child) order (C13) and
-//      the next frontier (PED, used bitmask, lambda row) is written with coalesced word copies.
-// After the last level, each survivor gets the insertion completion (C6) and the
+//      cnt_p(u) = popc(adj2[u] & used_p), cB_p(u) = popc(adj2[u] & B_p).  Each child is written as
+//      a one-byte rank code (PED - base + 1, saturated) to shared memory and counted in a 256-bin
+//      shared histogram (warp-aggregated with match.any).  Children never reach HBM.
+//   T  Threshold (replaces the paper's local/global ranking): a warp scan of the
+//      histogram gives the threshold PED t and the quota r of ties at t; exactly min(K, c_i)
+//      children are kept, the smallest under (PED, parent, child) (reading C12).  No sort.
+//   S  Selection: every thread owns a contiguous run of code words; SIMD byte compares count
+//      codes < t / == t, a block scan gives each thread its output offset and tie admissions,
+//      and survivors are written in (parent, child) order (C13).
+//   U  Update: the next frontier columns are written with coalesced stores.
+// After the last level each survivor gets the insertion completion (C6) and the
 // argmin by (total, position) is written out (C10).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace fg {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int MAP_DEL = 255;     // lambda entry of a deleted g1 vertex
+constexpr int MAP_DEL = 255;      // lambda entry of a deleted g1 vertex
 constexpr int CODE_INVALID = 255; // no child in this slot (used target / padding)
+constexpr int DMAX = 8;           // labelled path: lambda images of P_i staged per parent
 
 struct Costs {
     int vsub, vdel, vins, esub, edel, eins;
@@ -46,6 +54,13 @@ struct PairDesc {
     int64_t map_out;             // element offset of this pair's mapping in the output array
 };
 
+// Work-array plan of a batched launch.  pq/pl/e2: byte offsets into dynamic shared memory.
+// ped/u/b/t/codes/sel: byte offsets into shared memory (SMEM launches) or into the CTA's global
+// scratch after its two frontier buffers (large-K launches).
+struct SmemPlan {
+    int32_t pq, pl, e2, ped, u, b, t, codes, sel, bytes;
+};
+
 struct BatchArgs {
     const PairDesc *descs;
     const int32_t *order;   // pair indices of this launch, in scheduling order
@@ -53,15 +68,14 @@ struct BatchArgs {
     const uint8_t *blob;
     int32_t *work;          // dynamic scheduler counter (zeroed before launch)
     Costs c;
-    int32_t K;
+    int32_t K;              // the K of Alg. 1 (children kept per level)
+    int32_t Kc;             // frontier capacity / array stride (>= min(K, widest level), multiple of 4)
     int32_t win;            // exact rank window: codes 1..win; win+1 = saturated
-    int32_t n1s;            // lambda row stride in bytes (multiple of 4, >= max n1)
-    int32_t n1max;          // max n1 in this launch (P-list smem size)
-    int32_t csmax;          // max code row stride
-    int32_t e2bytes;        // smem bytes for e2lab (labelled launches)
-    int32_t codes_in_smem, sel_in_smem;
-    uint8_t *scratch;       // per-CTA frontier / code / selection scratch
+    int32_t csmax;          // max code row stride of the launch
+    SmemPlan sm;
+    uint8_t *scratch;       // per-CTA frontier scratch
     int64_t scratch_stride;
+    int32_t n1max;
     int64_t *cost_out;
     int32_t *map_out;
     int64_t *children_out;
@@ -76,76 +90,85 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-template <int W>
-struct FrontierView {
-    int32_t *ped;
-    uint32_t *used;
-    uint8_t *map;
-};
-
-// Scalar recomputation of one child's PED (used when its rank code was saturated; rare).
-template <int W, bool LAB>
-__device__ int child_ped_scalar(const Costs &c, int pedp, const uint32_t *Up, const uint8_t *mrow, int j,
-                                int n2, int n2p, int d, const int32_t *s_pq, const int32_t *s_pl,
-                                int vl1i, const int32_t *vl2, const uint32_t *adj2, const uint8_t *s_e2) {
-    if (j == n2) return pedp + c.vdel + c.edel * d;
-    int cv = (vl2[j] == vl1i) ? 0 : c.vsub;
-    int cnt = 0, cb = 0, mis = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) cnt += __popc(adj2[j * W + w] & Up[w]);
-    for (int k = 0; k < d; ++k) {
-        int t = mrow[s_pq[k]];
-        if (t == MAP_DEL) continue;
-        if (!LAB) {
-            cb += (adj2[j * W + (t >> 5)] >> (t & 31)) & 1u;
-        } else {
-            int e = s_e2[t * n2p + j];
-            cb += (e != 0);
-            mis += (e != 0) & (e != s_pl[k]);
-        }
-    }
-    return pedp + cv + c.edel * d + c.eins * cnt - (c.edel + c.eins) * cb + c.esub * mis;
+// Block barrier preceded by warp reconvergence: __syncthreads() is bar.sync (an .aligned barrier),
+// so every warp must arrive converged -- after lane-divergent code (lane 0 writing shared state)
+// the warp is reconverged explicitly first.
+__device__ __forceinline__ void block_sync() {
+    __syncwarp();
+    __syncthreads();
 }
 
-template <int W, bool LAB>
-__global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
+__device__ __forceinline__ int rank_code(int ped, int base, int win) {
+    const int x = ped - base + 1;
+    return x < 0 ? 0 : (x > win ? win + 1 : x);
+}
+
+// Block-wide exclusive scan of two ints (NT threads).  Returns totals.
+template <int NT>
+__device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, int &atot, int &btot, int *s_tmp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int xa = __shfl_up_sync(FULL, ia, o), xb = __shfl_up_sync(FULL, ib, o);
+        if (lane >= o) { ia += xa; ib += xb; }
+    }
+    if (lane == 31) { s_tmp[warp] = ia; s_tmp[32 + warp] = ib; }
+    block_sync();
+    if (warp == 0) {
+        int wa = lane < NT / 32 ? s_tmp[lane] : 0, wb = lane < NT / 32 ? s_tmp[32 + lane] : 0;
+        int sa = wa, sb = wb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int xa = __shfl_up_sync(FULL, sa, o), xb = __shfl_up_sync(FULL, sb, o);
+            if (lane >= o) { sa += xa; sb += xb; }
+        }
+        s_tmp[64 + lane] = sa - wa;
+        s_tmp[96 + lane] = sb - wb;
+        if (lane == 31) { s_tmp[128] = sa; s_tmp[129] = sb; }
+    }
+    block_sync();
+    apre = s_tmp[64 + warp] + ia - a;
+    bpre = s_tmp[96 + warp] + ib - b;
+    atot = s_tmp[128];
+    btot = s_tmp[129];
+}
+
+template <int W, bool LAB, int NT, bool SMEM>
+__global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
-    __shared__ int s_hist[256];
-    __shared__ int s_wcnt[32], s_wlt[32], s_weq[32], s_weqpre[32], s_wout[32];
-    __shared__ int s_item, s_keepall, s_tcode, s_r, s_retry, s_nnext, s_lo, s_below_add;
-    __shared__ int64_t s_ci;
+    __shared__ int s_hist[(NT / 32) * 129];
+    __shared__ int s_tmp[176];
+    __shared__ int s_item, s_lo;
     __shared__ unsigned long long s_best;
+    constexpr int NW = NT / 32;
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Costs c = a.c;
-    const int K = a.K, win = a.win, n1s = a.n1s;
+    const int K = a.K, Kc = a.Kc, win = a.win;
 
-    // dynamic smem carve: P list, e2lab, codes (optional), sel (optional)
-    int32_t *s_pq = reinterpret_cast<int32_t *>(dsmem);
-    int32_t *s_pl = s_pq + a.n1max;
-    uint8_t *s_e2 = reinterpret_cast<uint8_t *>(s_pl + a.n1max);
-    uint8_t *sm_next = s_e2 + a.e2bytes;
-
-    // per-CTA scratch carve (global)
+    // per-CTA frontier (two buffers): ped[K], usedT[W][K], mapT[n1max][K]
     uint8_t *scr = a.scratch + (int64_t)blockIdx.x * a.scratch_stride;
-    FrontierView<W> F[2];
-    F[0].ped = reinterpret_cast<int32_t *>(scr);
-    F[1].ped = F[0].ped + K;
-    F[0].used = reinterpret_cast<uint32_t *>(F[1].ped + K);
-    F[1].used = F[0].used + (int64_t)K * W;
-    F[0].map = reinterpret_cast<uint8_t *>(F[1].used + (int64_t)K * W);
-    F[1].map = F[0].map + (int64_t)K * n1s;
-    uint8_t *gnext = F[1].map + (int64_t)K * n1s;
-    uint8_t *codes;
-    uint32_t *sel;
-    if (a.codes_in_smem) { codes = sm_next; sm_next += ((int64_t)K * a.csmax + 15) & ~15ll; }
-    else { codes = gnext; gnext += ((int64_t)K * a.csmax + 15) & ~15ll; }
-    if (a.sel_in_smem) sel = reinterpret_cast<uint32_t *>(sm_next);
-    else sel = reinterpret_cast<uint32_t *>(gnext);
+    const int64_t fb = (int64_t)Kc * (4 + 4 * W + a.n1max); // bytes per frontier buffer
+    // per-level work arrays: shared memory (SMEM) or, for large K, this CTA's global scratch
+    uint8_t *wk = SMEM ? dsmem : scr + 2 * fb;
+    int32_t *s_pq = reinterpret_cast<int32_t *>(dsmem + a.sm.pq);
+    int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
+    uint8_t *s_e2 = dsmem + a.sm.e2;
+    int32_t *sPed = reinterpret_cast<int32_t *>(wk + a.sm.ped);
+    uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);
+    uint32_t *sB = reinterpret_cast<uint32_t *>(wk + a.sm.b);
+    uint8_t *sT = wk + a.sm.t;
+    uint8_t *codes = wk + a.sm.codes;
+    uint32_t *sel = reinterpret_cast<uint32_t *>(wk + a.sm.sel);
+
+    auto fped = [&](int b) { return reinterpret_cast<int32_t *>(scr + b * fb); };
+    auto fused = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + 4 * (int64_t)Kc); };
+    auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 4 * W); };
 
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
-        __syncthreads();
+        block_sync();
         const int item = s_item;
         if (item >= a.ngroup) return;
         const PairDesc pd = a.descs[a.order[item]];
@@ -163,7 +186,7 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
         int vl2r[W];
 #pragma unroll
         for (int s = 0; s < W; ++s) {
-            int u = lane + 32 * s;
+            const int u = lane + 32 * s;
 #pragma unroll
             for (int w = 0; w < W; ++w) A[s][w] = (u < n2) ? __ldg(adj2 + u * W + w) : 0u;
             vl2r[s] = (u < n2) ? __ldg(vl2 + u) : 0;
@@ -171,56 +194,82 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
         if (LAB) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
             uint32_t *dst = reinterpret_cast<uint32_t *>(s_e2);
-            for (int x = threadIdx.x; x < n2p * n2p / 4; x += blockDim.x) dst[x] = __ldg(src + x);
+            for (int x = threadIdx.x; x < n2p * n2p / 4; x += NT) dst[x] = __ldg(src + x);
         }
         // root node: lambda empty, all of V2 remaining, PED 0
-        if (threadIdx.x == 0) F[0].ped[0] = 0;
-        if (threadIdx.x < W) F[0].used[threadIdx.x] = 0u;
+        if (threadIdx.x == 0) fped(0)[0] = 0;
+        if (threadIdx.x < W) fused(0)[(int64_t)threadIdx.x * Kc] = 0u;
         int N = 1, lo = 0, cur = 0;
         int64_t children = 0, parents = 0, algb = 0;
 
         for (int i = 0; i < n1; ++i) {
-            const FrontierView<W> P = F[cur], Q = F[cur ^ 1];
+            const int32_t *Pped = fped(cur);
+            const uint32_t *PusedT = fused(cur);
+            const uint8_t *PmapT = fmap(cur);
+            int32_t *Qped = fped(cur ^ 1);
+            uint32_t *QusedT = fused(cur ^ 1);
+            uint8_t *QmapT = fmap(cur ^ 1);
             const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
-            for (int k = threadIdx.x; k < d; k += blockDim.x) {
+            for (int k = threadIdx.x; k < d; k += NT) {
                 s_pq[k] = __ldg(pq + pbeg + k);
                 s_pl[k] = __ldg(pl + pbeg + k);
             }
-            for (int k = threadIdx.x; k < 256; k += blockDim.x) s_hist[k] = 0;
+            for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
             const int vl1i = __ldg(vl1 + i);
             int cv[W];
 #pragma unroll
             for (int s = 0; s < W; ++s) cv[s] = (vl2r[s] == vl1i) ? 0 : c.vsub;
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
-            const int chunk = (N + NW - 1) / NW;
-            const int p0 = min(N, warp * chunk), p1 = min(N, p0 + chunk);
-            int base = lo, below = 0;
-            bool first = true;
-            __syncthreads();
+            block_sync();
+
+            // ---------------- P: parent prepass (coalesced over parents) ----------------
+            for (int p = threadIdx.x; p < N; p += NT) {
+                sPed[p] = Pped[p];
+#pragma unroll
+                for (int w = 0; w < W; ++w) sU[p * W + w] = PusedT[(int64_t)w * Kc + p];
+                if (!LAB) {
+                    uint32_t B[W];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) B[w] = 0u;
+#pragma unroll 4
+                    for (int k = 0; k < d; ++k) {
+                        const int t = PmapT[(int64_t)s_pq[k] * Kc + p];
+#pragma unroll
+                        for (int w = 0; w < W; ++w)
+                            B[w] |= (t != MAP_DEL && (t >> 5) == w) ? (1u << (t & 31)) : 0u;
+                    }
+#pragma unroll
+                    for (int w = 0; w < W; ++w) sB[p * W + w] = B[w];
+                } else {
+                    const int dd = min(d, DMAX);
+                    for (int k = 0; k < dd; ++k) sT[k * Kc + p] = PmapT[(int64_t)s_pq[k] * Kc + p];
+                }
+            }
+            block_sync();
 
             // ---------------- A + T: branch, rank codes, histogram, threshold ----------------
+            const int chunk = (N + NW - 1) / NW;
+            const int p0 = min(N, warp * chunk), p1 = min(N, p0 + chunk);
+            int base = lo, below = 0, ci = 0, tcode = 256, rq = 0, below_add = 0;
+            bool first = true, keepall = false, retry = false;
+            // exact histogram of rank codes 1..win (win <= 128): one private row per warp, shared atomics
+            int *whist = s_hist + warp * 129;
             for (;;) {
                 int wcount = 0;
+                auto hist_add = [&](int code) {
+                    if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
+                };
                 for (int p = p0; p < p1; ++p) {
-                    const int pedp = P.ped[p];
+                    const int pedp = sPed[p];
                     uint32_t U[W];
+                    int usedc = 0;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) U[w] = P.used[(int64_t)p * W + w];
-                    const uint8_t *mrow = P.map + (int64_t)p * n1s;
+                    for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; usedc += __popc(U[w]); }
                     int ped_s[W];
                     if (!LAB) {
                         uint32_t B[W];
 #pragma unroll
-                        for (int w = 0; w < W; ++w) B[w] = 0u;
-                        for (int k0 = 0; k0 < d; k0 += 32) {
-                            const int k = k0 + lane;
-                            const int t = (k < d) ? mrow[s_pq[k]] : MAP_DEL;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) {
-                                const unsigned bit = (t != MAP_DEL && (t >> 5) == w) ? (1u << (t & 31)) : 0u;
-                                B[w] |= __reduce_or_sync(FULL, bit);
-                            }
-                        }
+                        for (int w = 0; w < W; ++w) B[w] = sB[p * W + w];
 #pragma unroll
                         for (int s = 0; s < W; ++s) {
                             int cnt = 0, cb = 0;
@@ -235,22 +284,17 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
                         int cb[W], mis[W];
 #pragma unroll
                         for (int s = 0; s < W; ++s) { cb[s] = 0; mis[s] = 0; }
-                        for (int k0 = 0; k0 < d; k0 += 32) {
-                            const int k = k0 + lane;
-                            int t = MAP_DEL, l = 0;
-                            if (k < d) { t = mrow[s_pq[k]]; l = s_pl[k]; }
-                            const int kn = min(32, d - k0);
-                            for (int kk = 0; kk < kn; ++kk) {
-                                const int tt = __shfl_sync(FULL, t, kk), ll = __shfl_sync(FULL, l, kk);
-                                if (tt == MAP_DEL) continue;
-                                const uint8_t *row = s_e2 + tt * n2p;
+                        for (int k = 0; k < d; ++k) {
+                            const int tt = (k < DMAX) ? sT[k * Kc + p] : PmapT[(int64_t)s_pq[k] * Kc + p];
+                            if (tt == MAP_DEL) continue;
+                            const int ll = s_pl[k];
+                            const uint8_t *row = s_e2 + tt * n2p;
 #pragma unroll
-                                for (int s = 0; s < W; ++s) {
-                                    const int u = lane + 32 * s;
-                                    const int e = (u < n2p) ? row[u] : 0;
-                                    cb[s] += (e != 0);
-                                    mis[s] += (e != 0) & (e != ll);
-                                }
+                            for (int s = 0; s < W; ++s) {
+                                const int u = lane + 32 * s;
+                                const int e = (u < n2p) ? row[u] : 0;
+                                cb[s] += (e != 0);
+                                mis[s] += (e != 0) & (e != ll);
                             }
                         }
 #pragma unroll
@@ -262,168 +306,204 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
                         }
                     }
                     const int pedD = pedp + dDel;
-                    uint8_t *crow = codes + (int64_t)p * cs;
-                    int nvalid = 1; // the deletion child always exists (C5)
+                    uint8_t *crow = codes + p * cs;
 #pragma unroll
                     for (int s = 0; s < W; ++s) {
                         const int u = lane + 32 * s;
                         const bool sub = (u < n2) && !((U[s] >> lane) & 1u);
                         const bool del = (u == n2);
                         int code = CODE_INVALID;
-                        if (sub || del) {
-                            const int x = (sub ? ped_s[s] : pedD) - base + 1;
-                            code = x < 0 ? 0 : (x > win ? win + 1 : x);
-                            if (code >= 1 && code <= win) atomicAdd(&s_hist[code], 1);
-                        }
+                        if (sub || del) code = rank_code(sub ? ped_s[s] : pedD, base, win);
+                        hist_add(code);
                         if (u < cs) crow[u] = (uint8_t)code;
-                        nvalid += __popc(__ballot_sync(FULL, sub));
                     }
                     if (32 * W < cs) { // n2 == 32 W: the deletion slot lies past the lane slots
                         const int u = 32 * W + lane;
-                        if (u < cs) {
-                            int code = CODE_INVALID;
-                            if (u == n2) {
-                                const int x = pedD - base + 1;
-                                code = x < 0 ? 0 : (x > win ? win + 1 : x);
-                                if (code >= 1 && code <= win) atomicAdd(&s_hist[code], 1);
-                            }
-                            crow[u] = (uint8_t)code;
-                        }
+                        const int code = (u == n2) ? rank_code(pedD, base, win) : CODE_INVALID;
+                        hist_add(code);
+                        if (u < cs) crow[u] = (uint8_t)code;
                     }
-                    wcount += nvalid;
+                    wcount += n2 - usedc + 1; // |R_V2| substitutions + the deletion (C5)
                 }
-                if (first && lane == 0) s_wcnt[warp] = wcount;
-                __syncthreads();
-                if (threadIdx.x == 0) {
+                if (first && lane == 0) s_tmp[144 + warp] = wcount; // (block_scan2 owns s_tmp[0..130))
+                block_sync();
+                { // T: every warp derives the same threshold from the per-warp histograms (4 codes per lane)
                     if (first) {
-                        int64_t ci = 0;
-                        for (int w = 0; w < NW; ++w) ci += s_wcnt[w];
-                        s_ci = ci;
-                        s_keepall = (ci <= K);
+                        ci = lane < NW ? s_tmp[144 + lane] : 0;
+                        ci = __reduce_add_sync(FULL, ci);
                     }
-                    s_retry = 0;
-                    if (!s_keepall) {
-                        int cum = below, t = 0;
-                        for (int b = 1; b <= win; ++b) {
-                            if (cum + s_hist[b] >= K) { t = b; break; }
-                            cum += s_hist[b];
+                    keepall = ci <= K;
+                    int hv[4], sum = 0;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const int bb = 4 * lane + 1 + x; // codes 1..128
+                        int v = 0;
+                        if (bb <= win)
+                            for (int w = 0; w < NW; ++w) v += s_hist[w * 129 + bb];
+                        hv[x] = v;
+                        sum += v;
+                    }
+                    int incl = sum;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const unsigned hm = __ballot_sync(FULL, !keepall && (below + incl >= K));
+                    const int total = __shfl_sync(FULL, incl, 31);
+                    retry = !keepall && hm == 0u;
+                    int tc = 0, rr = 0;
+                    if (hm) {
+                        const int L = __ffs(hm) - 1;
+                        int cum = below + incl - sum;
+                        int c2 = cum;
+                        tc = 0;
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            if (tc == 0 && c2 + hv[x] >= K) { tc = 4 * lane + 1 + x; rr = K - c2; }
+                            c2 += hv[x];
                         }
-                        if (t) { s_tcode = t; s_r = K - cum; }
-                        else { s_retry = 1; s_below_add = cum - below; }
+                        tcode = __shfl_sync(FULL, tc, L);
+                        rq = __shfl_sync(FULL, rr, L);
                     }
+                    below_add = total;
                 }
-                __syncthreads();
-                if (!s_retry) break;
+                if (!retry) break; // (uniform: every warp computed the same value)
                 // the K-th smallest PED lies beyond the window: slide it (all codes < base are kept)
-                below += s_below_add;
+                block_sync(); // all warps have read the histograms
+                below += below_add;
                 base += win;
                 first = false;
-                for (int k = threadIdx.x; k < 256; k += blockDim.x) s_hist[k] = 0;
-                __syncthreads();
+                for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
+                block_sync();
             }
-            const bool keepall = s_keepall;
-            const int tcode = s_tcode, rq = s_r;
 
-            // ---------------- B: per-warp counts below / at the threshold ----------------
+            // ---------------- S: exact threshold + selection by segment scan over the code words ----------------
+            int Nn;
             {
+                const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes);
+                const int nwords = N * cs / 4;
+                const int seg = (nwords + NT - 1) / NT;
+                const int w0 = min(nwords, threadIdx.x * seg), w1 = min(nwords, w0 + seg);
+                if (keepall) { tcode = 256; rq = 0; }
+                // SWAR byte masks (codes are 0..win+1 <= 128 or 255): bit 7 of each byte set where
+                //   ge(t): byte >= t (t <= 128),  valid: byte != 255
+                const uint32_t t4 = (uint32_t)tcode * 0x01010101u, t41 = t4 + 0x01010101u;
+                auto ge = [](uint32_t x, uint32_t tt) { return (((x | 0x80808080u) - tt) | x) & 0x80808080u; };
+                auto valid = [](uint32_t x) { const uint32_t y = ~x; return (((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y) & 0x80808080u; };
                 int lt = 0, eq = 0;
-                const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes + (int64_t)p0 * cs);
-                const int nwords = (p1 - p0) * cs / 4;
-                const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
-                for (int x = lane; x < nwords; x += 32) {
+                for (int x = w0; x < w1; ++x) {
                     const uint32_t v = cw[x];
-                    if (keepall) lt += __popc(__vcmpne4(v, 0xffffffffu)) >> 3;
+                    if (keepall) lt += __popc(valid(v));
                     else {
-                        lt += __popc(__vcmpltu4(v, t4)) >> 3;
-                        eq += __popc(__vcmpeq4(v, t4)) >> 3;
+                        const int g0 = __popc(ge(v, t4));
+                        lt += 4 - g0;
+                        eq += g0 - __popc(ge(v, t41));
                     }
                 }
-                lt = __reduce_add_sync(FULL, lt);
-                eq = __reduce_add_sync(FULL, eq);
-                if (lane == 0) { s_wlt[warp] = lt; s_weq[warp] = eq; }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int eqpre = 0, out = 0;
-                for (int w = 0; w < NW; ++w) {
-                    int adm = keepall ? 0 : max(0, min(rq - eqpre, s_weq[w]));
-                    s_weqpre[w] = eqpre;
-                    s_wout[w] = out;
-                    out += s_wlt[w] + adm;
-                    eqpre += s_weq[w];
+                int ltpre, eqpre, lttot, eqtot;
+                block_scan2<NT>(lt, eq, ltpre, eqpre, lttot, eqtot, s_tmp);
+                Nn = keepall ? lttot : K;
+                int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
+                if (lt + eq > 0) {
+                    int pc = (4 * w0) / cs, uc = 4 * w0 - pc * cs;
+                    for (int x = w0; x < w1; ++x, uc += 4) {
+                        if (uc >= cs) { uc -= cs; ++pc; }
+                        const uint32_t v = cw[x];
+                        uint32_t mlt, meq = 0u;
+                        if (keepall) mlt = valid(v);
+                        else {
+                            const uint32_t g0 = ge(v, t4);
+                            mlt = ~g0 & 0x80808080u;
+                            meq = g0 & ~ge(v, t41);
+                        }
+                        uint32_t m = mlt | meq;
+                        while (m) {
+                            const int bit = __ffs(m) - 1, b = bit >> 3;
+                            m &= m - 1;
+                            bool keep = (mlt >> bit) & 1u;
+                            if (!keep) { keep = eq_seen < rq; eq_seen++; }
+                            if (keep) sel[out++] = ((uint32_t)pc << 8) | (uint32_t)(uc + b);
+                        }
+                    }
                 }
-                s_nnext = out;
-                s_lo = 0x7fffffff;
-                if (a.levels_out) {
-                    a.levels_out[3 * i] = N;
-                    a.levels_out[3 * i + 1] = s_ci;
-                    a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
-                }
-            }
-            __syncthreads();
-
-            // ---------------- C1: compact survivors in (parent, child) order ----------------
-            {
-                int eq_seen = s_weqpre[warp], out = s_wout[warp];
-                const unsigned lmask = lanemask_lt();
-                for (int p = p0; p < p1; ++p) {
-                    const uint8_t *crow = codes + (int64_t)p * cs;
-                    for (int u0 = 0; u0 < cs; u0 += 32) {
-                        const int u = u0 + lane;
-                        const int code = (u < cs) ? crow[u] : CODE_INVALID;
-                        const bool lt = keepall ? (code != CODE_INVALID) : (code < tcode);
-                        const bool eq = !keepall && (code == tcode);
-                        const unsigned eqm = __ballot_sync(FULL, eq);
-                        const bool keep = lt || (eq && (eq_seen + __popc(eqm & lmask)) < rq);
-                        const unsigned km = __ballot_sync(FULL, keep);
-                        if (keep) sel[out + __popc(km & lmask)] = ((uint32_t)p << 8) | (uint32_t)u;
-                        out += __popc(km);
-                        eq_seen += __popc(eqm);
+                if (threadIdx.x == 0) {
+                    s_lo = 0x7fffffff;
+                    if (a.levels_out) {
+                        a.levels_out[3 * i] = N;
+                        a.levels_out[3 * i + 1] = ci;
+                        a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
                     }
                 }
             }
-            __syncthreads();
-            const int Nn = s_nnext;
+            block_sync();
 
-            // ---------------- C2: write the next frontier ----------------
-            for (int k = threadIdx.x; k < Nn; k += blockDim.x) {
+            // ---------------- U: write the next frontier (coalesced over k) ----------------
+            for (int k = threadIdx.x; k < Nn; k += NT) {
                 const uint32_t v = sel[k];
                 const int p = (int)(v >> 8), j = (int)(v & 255u);
-                const int code = codes[(int64_t)p * cs + j];
-                uint32_t Up[W];
-#pragma unroll
-                for (int w = 0; w < W; ++w) Up[w] = P.used[(int64_t)p * W + w];
+                const int code = codes[p * cs + j];
                 int ped;
                 if (code >= 1 && code <= win) ped = base + code - 1;
-                else
-                    ped = child_ped_scalar<W, LAB>(c, P.ped[p], Up, P.map + (int64_t)p * n1s, j, n2, n2p, d,
-                                                   s_pq, s_pl, vl1i, vl2, adj2, s_e2);
-                Q.ped[k] = ped;
+                else { // saturated rank code: recompute the child's PED (rare)
+                    const int pedp = sPed[p];
+                    if (j == n2) ped = pedp + dDel;
+                    else {
+                        int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
-                for (int w = 0; w < W; ++w)
-                    Q.used[(int64_t)k * W + w] = Up[w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+                        for (int w = 0; w < W; ++w) cnt += __popc(__ldg(adj2 + j * W + w) & sU[p * W + w]);
+                        if (!LAB) {
+#pragma unroll
+                            for (int w = 0; w < W; ++w) cb += __popc(__ldg(adj2 + j * W + w) & sB[p * W + w]);
+                        } else {
+                            for (int q = 0; q < d; ++q) {
+                                const int t = (q < DMAX) ? sT[q * Kc + p] : PmapT[(int64_t)s_pq[q] * Kc + p];
+                                if (t == MAP_DEL) continue;
+                                const int e = s_e2[t * n2p + j];
+                                cb += (e != 0);
+                                mis += (e != 0) & (e != s_pl[q]);
+                            }
+                        }
+                        ped = pedp + ((__ldg(vl2 + j) == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - ee * cb + c.esub * mis;
+                    }
+                }
+                Qped[k] = ped;
                 atomicMin(&s_lo, ped);
             }
+            for (int x = threadIdx.x; x < W * Nn; x += NT) {
+                const int w = x / Nn, k = x - w * Nn;
+                const uint32_t v = sel[k];
+                const int p = (int)(v >> 8), j = (int)(v & 255u);
+                QusedT[(int64_t)w * Kc + k] = sU[p * W + w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+            }
             {
-                const int wpr = (i + 4) >> 2, hw = i >> 2, sh = (i & 3) * 8;
-                const int total = Nn * wpr;
-                for (int x = threadIdx.x; x < total; x += blockDim.x) {
-                    const int k = x / wpr, w = x - k * wpr;
-                    const uint32_t v = sel[k];
-                    const int p = (int)(v >> 8), j = (int)(v & 255u);
-                    uint32_t word = reinterpret_cast<const uint32_t *>(P.map + (int64_t)p * n1s)[w];
-                    if (w == hw) {
-                        const uint32_t e = (j == n2) ? (uint32_t)MAP_DEL : (uint32_t)j;
-                        word = (word & ~(0xffu << sh)) | (e << sh);
+                const int nk4 = (Nn + 3) >> 2;
+                for (int x = threadIdx.x; x < nk4; x += NT) {
+                    const int k0 = 4 * x;
+                    int pp[4];
+                    uint32_t last = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int k = min(k0 + b, Nn - 1);
+                        const uint32_t v = sel[k];
+                        pp[b] = (int)(v >> 8);
+                        const int j = (int)(v & 255u);
+                        last |= ((j == n2) ? (uint32_t)MAP_DEL : (uint32_t)j) << (8 * b);
                     }
-                    reinterpret_cast<uint32_t *>(Q.map + (int64_t)k * n1s)[w] = word;
+                    for (int q = 0; q < i; ++q) {
+                        const uint8_t *row = PmapT + (int64_t)q * Kc;
+                        const uint32_t word = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |
+                                              ((uint32_t)row[pp[2]] << 16) | ((uint32_t)row[pp[3]] << 24);
+                        *reinterpret_cast<uint32_t *>(QmapT + (int64_t)q * Kc + k0) = word;
+                    }
+                    *reinterpret_cast<uint32_t *>(QmapT + (int64_t)i * Kc + k0) = last;
                 }
             }
-            children += s_ci;
+            children += ci;
             parents += N;
-            // B_alg(i) = N_i (4 + b d_i) + N_{i+1} (b i + 4) + N_{i+1} (b (i+1) + 4), b = 1 (SURVEY §8(d) D.4)
+            // B_alg(i) = N_i (4 + b d_i) + N_{i+1} (b i + 4) + N_{i+1} (b (i+1) + 4), b = 1 (DESIGN.md §6)
             algb += (int64_t)N * (4 + d) + (int64_t)Nn * (2 * i + 9);
-            __syncthreads();
+            block_sync();
             N = Nn;
             lo = s_lo;
             cur ^= 1;
@@ -431,14 +511,15 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
 
         // ---------------- Finalize: insertion completion + argmin ----------------
         if (threadIdx.x == 0) s_best = ~0ull;
-        __syncthreads();
+        block_sync();
         {
-            const FrontierView<W> P = F[cur];
-            for (int k = threadIdx.x; k < N; k += blockDim.x) {
+            const int32_t *Pped = fped(cur);
+            const uint32_t *PusedT = fused(cur);
+            for (int k = threadIdx.x; k < N; k += NT) {
                 uint32_t U[W];
                 int usedc = 0, e2u2 = 0;
 #pragma unroll
-                for (int w = 0; w < W; ++w) { U[w] = P.used[(int64_t)k * W + w]; usedc += __popc(U[w]); }
+                for (int w = 0; w < W; ++w) { U[w] = PusedT[(int64_t)w * Kc + k]; usedc += __popc(U[w]); }
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     uint32_t bits = U[w];
@@ -450,16 +531,16 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
                         for (int x = 0; x < W; ++x) e2u2 += __popc(__ldg(adj2 + u * W + x) & U[x]);
                     }
                 }
-                const int64_t total = (int64_t)P.ped[k] + (int64_t)c.vins * (n2 - usedc) +
+                const int64_t total = (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) +
                                       (int64_t)c.eins * (pd.m2 - e2u2 / 2);
                 atomicMin(&s_best, ((unsigned long long)total << 32) | (unsigned)k);
             }
-            __syncthreads();
+            block_sync();
             const unsigned long long best = s_best;
             const int kb = (int)(best & 0xffffffffull);
-            const uint8_t *row = P.map + (int64_t)kb * n1s;
-            for (int q = threadIdx.x; q < n1; q += blockDim.x) {
-                const int t = row[q];
+            const uint8_t *PmapT = fmap(cur);
+            for (int q = threadIdx.x; q < n1; q += NT) {
+                const int t = PmapT[(int64_t)q * Kc + kb];
                 a.map_out[pd.map_out + q] = (t == MAP_DEL) ? -1 : t;
             }
             if (threadIdx.x == 0) {
@@ -470,7 +551,7 @@ __global__ void __launch_bounds__(256) kbest_batch_kernel(const BatchArgs a) {
                 a.algbytes_out[pidx] = algb;
             }
         }
-        __syncthreads();
+        block_sync();
     }
 }
 

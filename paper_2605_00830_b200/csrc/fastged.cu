@@ -133,6 +133,7 @@ struct fastged_handle {
     int evused = 0;
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     DevBuf lblob, lbuf; // large single-pair mode
+    fastged_batch *tmp = nullptr; // reused by solve_batch / solve_pair
 };
 
 namespace {
@@ -288,11 +289,15 @@ cudaEvent_t next_event(fastged_handle_t *h) {
 }
 
 // ---------------------------------------------------------------- batch build
+// Validates, packs and uploads a batch.  `reuse` (optional) is a batch whose device buffers are
+// recycled (solve_batch keeps one per handle, so repeated calls do no cudaMalloc/cudaFree).
 fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph_t *g1s,
-                           const fastged_graph_t *g2s) {
+                           const fastged_graph_t *g2s, fastged_batch *reuse = nullptr) {
     if (npairs < 0) fail(FASTGED_ERR_ARG, "npairs < 0");
     if (npairs > 0 && (!g1s || !g2s)) fail(FASTGED_ERR_ARG, "graph arrays are NULL");
-    fastged_batch *b = new fastged_batch();
+    fastged_batch *b = reuse ? reuse : new fastged_batch();
+    b->ran = false;
+    b->n1max = b->n2max = 0;
     try {
         b->npairs = npairs;
         b->descs.resize(npairs);
@@ -303,12 +308,26 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         std::vector<int64_t> off(npairs + 1);
         off[0] = 0;
         b->map_off[0] = 0;
+        // validation and sizing run in parallel over pairs (host cores); the first bad pair is reported
+        std::vector<int64_t> sz(npairs);
+        std::vector<FgError> perr(npairs > 0 ? 1 : 0);
+        int bad = npairs;
+#pragma omp parallel for schedule(dynamic, 64)
         for (int p = 0; p < npairs; ++p) {
-            validate_graph(&g1s[p], p, "g1");
-            validate_graph(&g2s[p], p, "g2");
-            lab[p] = labelled_pair(&g1s[p], &g2s[p]);
-            n2p[p] = (g2s[p].n + 3) & ~3;
-            off[p + 1] = off[p] + (int64_t)pair_blob_bytes(&g1s[p], &g2s[p], lab[p], n2p[p]);
+            try {
+                validate_graph(&g1s[p], p, "g1");
+                validate_graph(&g2s[p], p, "g2");
+                lab[p] = labelled_pair(&g1s[p], &g2s[p]);
+                n2p[p] = (g2s[p].n + 3) & ~3;
+                sz[p] = (int64_t)pair_blob_bytes(&g1s[p], &g2s[p], lab[p], n2p[p]);
+            } catch (const FgError &e) {
+#pragma omp critical(fg_err)
+                if (p < bad) { bad = p; perr[0] = e; }
+            }
+        }
+        if (bad < npairs) throw perr[0];
+        for (int p = 0; p < npairs; ++p) {
+            off[p + 1] = off[p] + sz[p];
             b->map_off[p + 1] = b->map_off[p] + g1s[p].n;
             b->n1max = std::max(b->n1max, g1s[p].n);
             b->n2max = std::max(b->n2max, g2s[p].n);
@@ -318,11 +337,18 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         size_t desc_bytes = sizeof(fg::PairDesc) * (size_t)std::max(npairs, 1);
         CK(h->stage.reserve(blob_bytes + desc_bytes + 64));
         uint8_t *stage = (uint8_t *)h->stage.p;
+#pragma omp parallel for schedule(dynamic, 64)
         for (int p = 0; p < npairs; ++p) {
-            pack_pair(&g1s[p], &g2s[p], lab[p], n2p[p], stage, off[p], b->descs[p], p);
+            try {
+                pack_pair(&g1s[p], &g2s[p], lab[p], n2p[p], stage, off[p], b->descs[p], p);
+            } catch (const FgError &e) {
+#pragma omp critical(fg_err)
+                if (p < bad) { bad = p; perr[0] = e; }
+            }
             b->descs[p].map_out = b->map_off[p];
             b->W[p] = words_for(g2s[p].n);
         }
+        if (bad < npairs) throw perr[0];
         memcpy(stage + blob_bytes, b->descs.data(), sizeof(fg::PairDesc) * (size_t)npairs);
         CK(b->blob.reserve(blob_bytes + 16));
         CK(b->ddesc.reserve(desc_bytes));
@@ -340,19 +366,36 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         CK(cudaStreamSynchronize(h->stream)); // staging buffer is reused by the next call
         return b;
     } catch (...) {
-        b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
-        b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
-        delete b;
+        if (!reuse) {
+            b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
+            b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
+            delete b;
+        }
         throw;
     }
 }
 
-template <int W, bool LAB>
-void launch_group(fastged_handle_t *h, fastged_batch *b, const fg::BatchArgs &args, int grid, size_t smem) {
-    auto kern = fg::kbest_batch_kernel<W, LAB>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 256, smem, h->stream>>>(args);
-    CK(cudaGetLastError());
+// Largest frontier any level can hold: N_{i+1} <= min(K, N_i (n2 + 1)), N_0 = 1.
+int64_t frontier_cap(int n1, int n2, int64_t k) {
+    int64_t N = 1, mx = 1;
+    for (int i = 0; i < n1 && N < k; ++i) {
+        N = std::min<int64_t>(k, N * (int64_t)(n2 + 1));
+        mx = std::max(mx, N);
+    }
+    return std::min(mx, k);
+}
+
+constexpr int BATCH_NT = 256;
+
+void *batch_kernel_for(int W, bool lab, bool smem) {
+#define KV(WW, LL, SS) \
+    if (W == WW && lab == LL && smem == SS) return (void *)fg::kbest_batch_kernel<WW, LL, BATCH_NT, SS>;
+    KV(1, false, true) KV(1, true, true) KV(2, false, true) KV(2, true, true)
+    KV(3, false, true) KV(3, true, true) KV(4, false, true) KV(4, true, true)
+    KV(1, false, false) KV(1, true, false) KV(2, false, false) KV(2, true, false)
+    KV(3, false, false) KV(3, true, false) KV(4, false, false) KV(4, true, false)
+#undef KV
+    return nullptr;
 }
 
 void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, int64_t k,
@@ -362,7 +405,6 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
     // group pairs by kernel variant; schedule the largest pairs first (dynamic counter)
     b->groups.clear();
     b->large.clear();
-    // host copies of the graphs are gone after upload; the descriptors hold the sizes
     for (int p = 0; p < b->npairs; ++p) {
         const fg::PairDesc &d = b->descs[p];
         int64_t bound = (int64_t)d.n1 * std::max(c->vsub, c->vdel) + (int64_t)d.n2 * c->vins +
@@ -405,12 +447,14 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         const GroupKey key = sp.first;
         const size_t start = sp.second.first, cnt = sp.second.second;
         int n1max = 0, n2max = 0;
+        int64_t kcap = 1;
         for (size_t x = start; x < start + cnt; ++x) {
-            n1max = std::max(n1max, b->descs[order_all[x]].n1);
-            n2max = std::max(n2max, b->descs[order_all[x]].n2);
+            const fg::PairDesc &d = b->descs[order_all[x]];
+            n1max = std::max(n1max, d.n1);
+            n2max = std::max(n2max, d.n2);
+            kcap = std::max(kcap, frontier_cap(d.n1, d.n2, k));
         }
         const int W = key.W;
-        const int K = (int)k;
         fg::BatchArgs a{};
         a.descs = (const fg::PairDesc *)b->ddesc.p;
         a.order = (const int32_t *)b->dorder.p + start;
@@ -418,46 +462,48 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.blob = (const uint8_t *)b->blob.p;
         a.work = (int32_t *)b->dwork.p + gi;
         a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
-        a.K = K;
-        a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
-        a.n1s = std::max(4, (n1max + 3) & ~3);
-        a.n1max = std::max(1, n1max);
+        a.K = (int)k;
+        a.Kc = (int)((kcap + 3) & ~3ll);
+        a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 127; // codes 0..128 (SWAR compares need <= 128)
+        a.n1max = std::max(4, (n1max + 3) & ~3);
         a.csmax = (n2max + 1 + 3) & ~3;
-        int n2p = (n2max + 3) & ~3;
-        a.e2bytes = key.lab ? (int)align16((size_t)n2p * n2p) : 0;
-        size_t codes_bytes = align16((size_t)K * a.csmax), sel_bytes = align16(4 * (size_t)K);
-        size_t smem = align16(8 * (size_t)a.n1max) + a.e2bytes;
-        a.codes_in_smem = (smem + codes_bytes <= 96 * 1024) ? 1 : 0;
-        if (a.codes_in_smem) smem += codes_bytes;
-        a.sel_in_smem = (smem + sel_bytes <= 112 * 1024) ? 1 : 0;
-        if (a.sel_in_smem) smem += sel_bytes;
-        if (smem > h->smem_optin - 4096) fail(FASTGED_ERR_CAPACITY, "shared memory plan too large");
-        // fix e2 carve: P list is 2 * n1max int32
-        size_t per_cta = 2 * 4 * (size_t)K + 2 * 4 * (size_t)K * W + 2 * (size_t)K * a.n1s;
-        if (!a.codes_in_smem) per_cta += codes_bytes;
-        if (!a.sel_in_smem) per_cta += sel_bytes;
-        per_cta = (per_cta + 255) & ~(size_t)255;
-        int occ = 0;
-        cudaError_t oe;
-        switch (W * 2 + (key.lab ? 1 : 0)) {
-#define OCC(WW, LL)                                                                                            \
-    case WW * 2 + LL:                                                                                          \
-        CK(cudaFuncSetAttribute(fg::kbest_batch_kernel<WW, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                (int)smem));                                                                   \
-        oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fg::kbest_batch_kernel<WW, LL>, 256, smem);    \
-        break;
-            OCC(1, 0) OCC(1, 1) OCC(2, 0) OCC(2, 1) OCC(3, 0) OCC(3, 1) OCC(4, 0) OCC(4, 1)
-#undef OCC
-        default: fail(FASTGED_ERR_ARG, "bad variant");
+        const size_t Kc = (size_t)a.Kc;
+        const int n2p = (n2max + 3) & ~3;
+        // always-shared small arrays
+        size_t sm = 0;
+        a.sm.pq = (int)sm; sm += align16(4 * (size_t)a.n1max);
+        a.sm.pl = (int)sm; sm += align16(4 * (size_t)a.n1max);
+        a.sm.e2 = (int)sm; sm += key.lab ? align16((size_t)n2p * n2p) : 0;
+        // per-level work arrays
+        size_t wk = 0;
+        auto put = [&](int32_t &field, size_t bytes) { field = (int)wk; wk += align16(bytes); };
+        put(a.sm.ped, 4 * Kc);
+        put(a.sm.u, 4 * Kc * W);
+        put(a.sm.b, 4 * Kc * W);
+        put(a.sm.t, key.lab ? (size_t)fg::DMAX * Kc : 0);
+        put(a.sm.codes, Kc * a.csmax);
+        put(a.sm.sel, 4 * Kc);
+        const bool in_smem = sm + wk + 8192 <= h->smem_optin;
+        size_t smem = sm;
+        if (in_smem) {
+            for (int32_t *f : {&a.sm.ped, &a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel}) *f += (int)sm;
+            smem += wk;
         }
-        CK(oe);
+        a.sm.bytes = (int)smem;
+        size_t per_cta = 2 * Kc * (4 + 4 * (size_t)W + a.n1max) + (in_smem ? 0 : wk);
+        per_cta = (per_cta + 255) & ~(size_t)255;
+        void *kern = batch_kernel_for(W, key.lab, in_smem);
+        if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BATCH_NT, smem));
         occ = std::max(occ, 1);
         int grid = (int)std::min<int64_t>((int64_t)cnt, (int64_t)occ * h->sms);
         // bound scratch to the device: shrink the grid, never K
-        size_t free_b = 0, total_b = 0;
-        CK(cudaMemGetInfo(&free_b, &total_b));
         size_t need = per_cta * (size_t)grid;
         if (need > h->scratch.cap) {
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
             size_t avail = free_b + h->scratch.cap;
             if (per_cta > avail / 2) fail(FASTGED_ERR_CAPACITY, "frontier scratch %zu B per CTA exceeds device memory", per_cta);
             while (grid > 1 && per_cta * (size_t)grid > avail * 3 / 4) grid--;
@@ -478,17 +524,8 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             e1 = next_event(h);
             CK(cudaEventRecord(e0, h->stream));
         }
-        switch (W * 2 + (key.lab ? 1 : 0)) {
-        case 2: launch_group<1, false>(h, b, a, grid, smem); break;
-        case 3: launch_group<1, true>(h, b, a, grid, smem); break;
-        case 4: launch_group<2, false>(h, b, a, grid, smem); break;
-        case 5: launch_group<2, true>(h, b, a, grid, smem); break;
-        case 6: launch_group<3, false>(h, b, a, grid, smem); break;
-        case 7: launch_group<3, true>(h, b, a, grid, smem); break;
-        case 8: launch_group<4, false>(h, b, a, grid, smem); break;
-        case 9: launch_group<4, true>(h, b, a, grid, smem); break;
-        default: fail(FASTGED_ERR_ARG, "bad variant");
-        }
+        void *params[] = {(void *)&a};
+        CK(cudaLaunchKernel(kern, dim3(grid), dim3(BATCH_NT), params, smem, h->stream));
         if (e1) CK(cudaEventRecord(e1, h->stream));
         h->stats.kernel_launches++;
         gi++;
@@ -557,16 +594,6 @@ void begin_call(fastged_handle_t *h) {
     CK(cudaSetDevice(h->device));
 }
 
-
-// Largest frontier any level can hold: N_{i+1} <= min(K, N_i (n2 + 1)), N_0 = 1.
-int64_t frontier_cap(int n1, int n2, int64_t k) {
-    int64_t N = 1, mx = 1;
-    for (int i = 0; i < n1 && N < k; ++i) {
-        N = std::min<int64_t>(k, N * (int64_t)(n2 + 1));
-        mx = std::max(mx, N);
-    }
-    return std::min(mx, k);
-}
 
 void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
                  const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out) {
@@ -736,6 +763,7 @@ void fastged_destroy(fastged_handle_t *h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     h->lblob.release();
     h->lbuf.release();
+    free_batch(h->tmp);
     h->scratch.release();
     h->levels.release();
     h->stage.release();
@@ -811,21 +839,20 @@ int fastged_solve_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph
                         const fastged_graph_t *g2s, const fastged_costs_t *c, int64_t k, int64_t *costs_out,
                         int32_t *mappings_out, int64_t *children_out) {
     if (!h) return FASTGED_ERR_ARG;
-    fastged_batch *b = nullptr;
     try {
         begin_call(h);
         validate_costs(c);
         if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
-        b = build_batch(h, npairs, g1s, g2s);
+        if (!h->tmp) h->tmp = new fastged_batch();
+        fastged_batch *b = build_batch(h, npairs, g1s, g2s, h->tmp);
         run_batch(h, b, c, k, nullptr);
         download(h, b, costs_out, mappings_out, children_out);
-        free_batch(b);
         return FASTGED_OK;
     } catch (const FgError &e) {
-        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        cudaStreamSynchronize(h->stream);
         return set_err(h, e);
     } catch (const std::bad_alloc &) {
-        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        cudaStreamSynchronize(h->stream);
         return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
     }
 }
@@ -847,7 +874,8 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }
-        b = build_batch(h, 1, g1, g2);
+        if (!h->tmp) h->tmp = new fastged_batch();
+        b = build_batch(h, 1, g1, g2, h->tmp);
         int64_t *lev = nullptr;
         if (levels_out && g1->n > 0) {
             CK(h->levels.reserve(24 * (size_t)g1->n));
@@ -861,13 +889,12 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
         out->children_evaluated = h->stats.children_evaluated;
         out->parents_expanded = h->stats.parents_expanded;
         out->device_ms = h->stats.device_ms;
-        free_batch(b);
         return FASTGED_OK;
     } catch (const FgError &e) {
-        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        if (b) cudaStreamSynchronize(h->stream);
         return set_err(h, e);
     } catch (const std::bad_alloc &) {
-        if (b) { cudaStreamSynchronize(h->stream); free_batch(b); }
+        if (b) cudaStreamSynchronize(h->stream);
         return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
     }
 }

@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         if (threadIdx.x == 0) a.ped[0][0] = 0;
         for (int w = threadIdx.x; w < W; w += blockDim.x) a.used[0][w] = 0u;
     }
-    __syncthreads();
-    grid.sync();
+    block_sync();
+    __syncwarp();
+        grid.sync();
 
     int N = 1, lo = 0, cur = 0, ps = 0;
     int64_t children = 0, parents = 0, algb = 0;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             if (threadIdx.x == 0) s_cnt = 0;
             if (blockIdx.x == 0)
                 for (int k = threadIdx.x; k < 256; k += blockDim.x) a.hist[((ps + 1) % 3) * 256 + k] = 0;
-            __syncthreads();
+            block_sync();
             int wcount = 0;
             for (int p = p0; p < p1; ++p) {
                 const int pedp = Pped[p];
@@ -205,12 +206,13 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
                 __syncwarp();
             }
             if (first && lane == 0) atomicAdd((unsigned long long *)&s_cnt, (unsigned long long)wcount);
-            __syncthreads();
+            block_sync();
             int *gh = a.hist + (ps % 3) * 256;
             for (int k = threadIdx.x; k < 256; k += blockDim.x)
                 if (s_hist[k]) atomicAdd(&gh[k], s_hist[k]);
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
-            grid.sync();
+            __syncwarp();
+        grid.sync();
             // T: every CTA derives the same threshold
             const int64_t ci = a.ci[i];
             keepall = (ci <= K);
@@ -227,11 +229,11 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
                     s_pre[0] = t;
                     s_pre[1] = t ? (K - cum) : (cum - below);
                 }
-                __syncthreads();
+                block_sync();
                 tcode = s_pre[0];
                 if (tcode) rq = s_pre[1];
                 else { retry = true; below += s_pre[1]; }
-                __syncthreads();
+                block_sync();
             }
             if (first) children += ci;
             ps++;
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             eq = __reduce_add_sync(FULL, eq);
             if (lane == 0) { a.wlt[gw] = lt; a.weq[gw] = eq; }
         }
+        __syncwarp();
         grid.sync();
 
         // ---------------- prefix for this CTA's warps (computed redundantly per CTA) ----------------
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             slt = __reduce_add_sync(FULL, slt);
             seq = __reduce_add_sync(FULL, seq);
             if (lane == 0) { s_red[0][wib] = slt; s_red[1][wib] = seq; }
-            __syncthreads();
+            block_sync();
         }
         int ltpre = 0, eqpre = 0;
         for (int w = 0; w < NWB; ++w) { ltpre += s_red[0][w]; eqpre += s_red[1][w]; }
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             a.levels_out[3 * i + 1] = a.ci[i];
             a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
         }
+        __syncwarp();
         grid.sync();
 
         // ---------------- C2: next frontier ----------------
@@ -347,6 +351,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         }
         parents += N;
         algb += (int64_t)N * (4 + (int)sizeof(MapT) * d) + (int64_t)Nn * ((int)sizeof(MapT) * (2 * i + 1) + 8);
+        __syncwarp();
         grid.sync();
         N = Nn;
         lo = a.lo[i + 1];
@@ -372,6 +377,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
                 atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)k);
             }
         }
+        __syncwarp();
         grid.sync();
         if (blockIdx.x == 0) {
             const unsigned long long best = *a.best;

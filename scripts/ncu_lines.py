@@ -1,0 +1,24 @@
+"""Aggregate an ncu '--page source --print-source cuda,sass' CSV by CUDA source line.
+usage: python scripts/ncu_lines.py report.ncu-rep [kernel-substring] [top]"""
+import csv, subprocess, sys, collections
+rep = sys.argv[1]; ksub = sys.argv[2] if len(sys.argv) > 2 else ""; top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+func = None; hdr = None; cur = None
+agg = collections.defaultdict(lambda: [0, 0, ""])
+for r in rows:
+    if not r: continue
+    if r[0] == "Function Name": func = r[1]; continue
+    if r[0] == "Line No": hdr = r; ix_inst = hdr.index("Instructions Executed"); ix_samp = hdr.index("Warp Stall Sampling (All Samples)"); continue
+    if r[0] == "File Path" or hdr is None: continue
+    if ksub and (func is None or ksub not in func): continue
+    if r[0] != "":
+        cur = (func, int(r[0])); agg[cur][2] = r[1][:90]; continue
+    try:
+        agg[cur][0] += int(float(r[ix_inst])); agg[cur][1] += int(float(r[ix_samp]))
+    except Exception:
+        pass
+tot_i = sum(v[0] for v in agg.values()) or 1; tot_s = sum(v[1] for v in agg.values()) or 1
+print(f"total warp-instructions {tot_i:.3e}, stall samples {tot_s}")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+    print(f"{100*v[1]/tot_s:5.1f}% samp {100*v[0]/tot_i:5.1f}% inst  L{k[1]:4d}  {v[2]}")
