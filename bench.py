@@ -161,7 +161,7 @@ def run_ours(args, rank, local_rank, world):
     clocks = ClockSampler(local_rank)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    branch_ms, branch_launches, launches, alg_bytes, children, parents, lib_ms = 0.0, 0, 0, 0, 0, 0, 0.0
+    branch_ms, branch_launches, launches, alg_bytes, children, parents, lib_ms, alg_ops = 0.0, 0, 0, 0, 0, 0, 0.0, 0
     barrier()
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()
@@ -177,6 +177,7 @@ def run_ours(args, rank, local_rank, world):
         branch_launches += st["branch_launches"]
         launches += st["kernel_launches"]
         alg_bytes += st["alg_bytes"]
+        alg_ops += st["alg_ops"]
         children += st["children_evaluated"]
         parents += st["parents_expanded"]
     torch.cuda.synchronize(dev)
@@ -221,7 +222,19 @@ def run_ours(args, rank, local_rank, world):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = (alg_bytes / args.steps) / (branch_ms / args.steps / 1e3) / 1e9 if branch_ms > 0 else None
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    # integer lane-op peak: 4 SMSPs x (16 ALU-pipe + 16 FMA-pipe lanes) per clock per SM
+    alu_peak = sms * 128 * clk_mhz * 1e6 / 1e9  # Gop/s
+    kern_s = branch_ms / args.steps / 1e3
+    achieved = (alg_ops / args.steps) / kern_s / 1e9 if branch_ms > 0 else None
+    hbm_ach = (alg_bytes / args.steps) / kern_s / 1e9 if branch_ms > 0 else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = prof.get("bench_kernel_dram_bytes_per_launch")
+    except Exception:
+        pass
     line = {
         "metric": METRIC,
         "value": value,
@@ -246,16 +259,19 @@ def run_ours(args, rank, local_rank, world):
             "l2": "256 MiB buffer written between timed steps (outside the CUDA-event region)",
         },
         "roofline": {
-            "bound": "hbm",
-            "kernel": "kbest_batch_kernel (branch+rank+update, all levels)",
+            "bound": "alu",
+            "kernel": "kbest_batch_kernel (branch+rank+update, all levels; one launch per word-width group)",
             "achieved": achieved,
-            "peak": hbm_peak,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback",
-            "unit": "GB/s",
-            "frac": (achieved / hbm_peak) if achieved else None,
-            "traffic": None,
-            "alg_bytes_per_step": alg_bytes / args.steps,
+            "peak": alu_peak,
+            "peak_source": f"derived: {sms} SMs x 128 int lanes/clk x {clk_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "unit": "Gop/s",
+            "frac": (achieved / alu_peak) if achieved else None,
+            "traffic": traffic,
+            "alg_ops_per_step": alg_ops / args.steps,
             "launches_per_step": branch_launches / args.steps,
+            "hbm_view": {"alg_bytes_per_step": alg_bytes / args.steps, "achieved_gbs": hbm_ach, "peak_gbs": hbm_peak,
+                         "frac": (hbm_ach / hbm_peak) if hbm_ach else None,
+                         "note": "frontier bytes each level touches (SURVEY §8(d) D.4); they stay in L2/SMEM"},
         },
         "e2e": {
             "value": pairs_total / e2e_max if e2e_max > 0 else None,

@@ -123,6 +123,8 @@ typedef struct {
     int64_t alg_bytes;            /* algorithmic frontier bytes of the search: sum over pairs and levels of
                                      N_i (4 + b d_i) + N_{i+1} (b i + 4) + N_{i+1} (b (i+1) + 4), b = bytes per
                                      lambda entry                                    */
+    int64_t alg_ops;              /* algorithmic integer lane-ops of the branch step: sum over children of
+                                     4 W + 8, W = ceil(n2 / 32) words per bit row     */
 } fastged_stats_t;
 
 /* Create a handle.  Returns FASTGED_ERR_CUDA if the device cannot be used, FASTGED_ERR_NCCL if the

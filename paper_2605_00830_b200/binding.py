@@ -62,7 +62,7 @@ class StatsT(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("device_ms", C.c_float), ("branch_ms", C.c_float),
                 ("branch_launches", C.c_int64), ("children_evaluated", C.c_int64),
                 ("parents_expanded", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("alg_bytes", C.c_int64)]
+                ("alg_bytes", C.c_int64), ("alg_ops", C.c_int64)]
 
 
 _lib = None

@@ -138,7 +138,7 @@ template <int W, bool LAB, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     __shared__ int s_hist[(NT / 32) * 129];
-    __shared__ int s_tmp[176];
+    __shared__ int s_tmp[144 + 32];
     __shared__ int s_item, s_lo;
     __shared__ unsigned long long s_best;
     constexpr int NW = NT / 32;
@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         const int j = (int)(v & 255u);
                         last |= ((j == n2) ? (uint32_t)MAP_DEL : (uint32_t)j) << (8 * b);
                     }
+#pragma unroll 4
                     for (int q = 0; q < i; ++q) {
                         const uint8_t *row = PmapT + (int64_t)q * Kc;
                         const uint32_t word = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |

@@ -574,11 +574,15 @@ void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t
     if (P) memcpy(costs_out, hc, 8 * P);
     if (M) memcpy(mappings_out, hm, 4 * M);
     if (children_out && P) memcpy(children_out, hch, 8 * P);
-    int64_t ch = 0, pa = 0, al = 0;
-    for (size_t p = 0; p < P; ++p) { ch += hch[p]; pa += hpa[p]; al += hal[p]; }
+    int64_t ch = 0, pa = 0, al = 0, ops = 0;
+    for (size_t p = 0; p < P; ++p) {
+        ch += hch[p]; pa += hpa[p]; al += hal[p];
+        ops += hch[p] * (4 * (int64_t)b->W[p] + 8); // popcount-form lane-ops per child
+    }
     h->stats.children_evaluated = ch;
     h->stats.parents_expanded = pa;
     h->stats.alg_bytes = al;
+    h->stats.alg_ops = ops;
 }
 
 void free_batch(fastged_batch *b) {
@@ -695,6 +699,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     h->stats.children_evaluated = res[1];
     h->stats.parents_expanded = res[2];
     h->stats.alg_bytes = res[3];
+    h->stats.alg_ops = res[1] * (4 * (int64_t)W + 8);
     h->stats.d2h_bytes += 32 + 4 * (int64_t)n1;
     out->cost = res[0];
     out->children_evaluated = res[1];

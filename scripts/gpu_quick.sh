@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
+python scripts/prof_batch.py 10000 1000 2 2>&1 | tail -1
