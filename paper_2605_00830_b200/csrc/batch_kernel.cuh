@@ -58,7 +58,7 @@ struct PairDesc {
 // ped/u/b/t/codes/sel: byte offsets into shared memory (SMEM launches) or into the CTA's global
 // scratch after its two frontier buffers (large-K launches).
 struct SmemPlan {
-    int32_t pq, pl, e2, ped, u, b, t, codes, sel, bytes;
+    int32_t pq, pl, e2, adj, ped, u, b, t, codes, sel, bytes;
 };
 
 struct BatchArgs {
@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
     int32_t *s_pq = reinterpret_cast<int32_t *>(dsmem + a.sm.pq);
     int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
     uint8_t *s_e2 = dsmem + a.sm.e2;
+    uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
     int32_t *sPed = reinterpret_cast<int32_t *>(wk + a.sm.ped);
     uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);
     uint32_t *sB = reinterpret_cast<uint32_t *>(wk + a.sm.b);
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             for (int w = 0; w < W; ++w) A[s][w] = (u < n2) ? __ldg(adj2 + u * W + w) : 0u;
             vl2r[s] = (u < n2) ? __ldg(vl2 + u) : 0;
         }
+        for (int x = threadIdx.x; x < n2 * W; x += NT) sAdj[x] = __ldg(adj2 + x);
         if (LAB) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
             uint32_t *dst = reinterpret_cast<uint32_t *>(s_e2);
@@ -259,6 +261,51 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                 auto hist_add = [&](int code) {
                     if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
                 };
+                const bool tpp = !LAB && N >= NT / 2;
+                if (tpp) {
+                    // wide frontier: thread per parent, iterating only the parent's free targets (no idle lanes)
+                    uint32_t Mm[W], Vm[W];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        Vm[w] = __ballot_sync(FULL, lane + 32 * w < n2);                   // targets that exist
+                        Mm[w] = __ballot_sync(FULL, lane + 32 * w < n2 && vl2r[w] != vl1i); // label mismatches
+                    }
+                    for (int p = threadIdx.x; p < N; p += NT) {
+                        const int pedp = sPed[p];
+                        uint32_t U[W], B[W];
+#pragma unroll
+                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = sB[p * W + w]; }
+                        uint8_t *crow = codes + p * cs;
+                        for (int x = 0; x < cs / 4; ++x) reinterpret_cast<uint32_t *>(crow)[x] = 0xffffffffu;
+                        const int cdel = rank_code(pedp + dDel, base, win); // deletion child (C5)
+                        crow[n2] = (uint8_t)cdel;
+                        hist_add(cdel);
+                        int nf = 1;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            uint32_t F = Vm[w] & ~U[w];
+                            nf += __popc(F);
+                            while (F) {
+                                const int bt = __ffs(F) - 1;
+                                F &= F - 1;
+                                const int u = 32 * w + bt;
+                                int cnt = 0, cb = 0;
+#pragma unroll
+                                for (int x = 0; x < W; ++x) {
+                                    const uint32_t r = sAdj[u * W + x];
+                                    cnt += __popc(r & U[x]);
+                                    cb += __popc(r & B[x]);
+                                }
+                                const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb;
+                                const int code = rank_code(ped, base, win);
+                                crow[u] = (uint8_t)code;
+                                hist_add(code);
+                            }
+                        }
+                        wcount += nf;
+                    }
+                    wcount = __reduce_add_sync(FULL, wcount);
+                } else
                 for (int p = p0; p < p1; ++p) {
                     const int pedp = sPed[p];
                     uint32_t U[W];
