@@ -90,12 +90,31 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-// Block barrier preceded by warp reconvergence: __syncthreads() is bar.sync (an .aligned barrier),
-// so every warp must arrive converged -- after lane-divergent code (lane 0 writing shared state)
-// the warp is reconverged explicitly first.
+// Block barrier that is safe after lane-divergent code.  __syncthreads() compiles to bar.sync, an
+// .aligned barrier that requires every warp to arrive converged; ptxas may drop a preceding
+// __syncwarp(), and a warp leaving a strided loop with unequal trip counts then reaches the
+// barrier diverged (undefined behaviour, seen as out-of-phase warps under compute-sanitizer
+// synccheck).  The non-aligned barrier.sync is defined for divergent arrival; the explicit
+// bar.warp.sync (volatile asm, cannot be elided) reconverges the warp for the code that follows.
 __device__ __forceinline__ void block_sync() {
-    __syncwarp();
-    __syncthreads();
+    asm volatile("bar.warp.sync -1;" ::: "memory");
+#ifdef FG_ALIGNED_BARRIER
+    asm volatile("bar.sync 0;" ::: "memory");
+#else
+    asm volatile("barrier.sync 0;" ::: "memory");
+    asm volatile("bar.warp.sync -1;" ::: "memory");
+#endif
+}
+
+// Position of the (r+1)-th set bit of x (0 <= r < popc(x)): popcount bisection, no data-dependent loop.
+__device__ __forceinline__ int select_bit(uint32_t x, int r) {
+    int pos = 0, c;
+    c = __popc(x & 0xffffu); if (r >= c) { r -= c; x >>= 16; pos += 16; }
+    c = __popc(x & 0xffu);   if (r >= c) { r -= c; x >>= 8;  pos += 8; }
+    c = __popc(x & 0xfu);    if (r >= c) { r -= c; x >>= 4;  pos += 4; }
+    c = __popc(x & 0x3u);    if (r >= c) { r -= c; x >>= 2;  pos += 2; }
+    c = (int)(x & 1u);       if (r >= c) { pos += 1; }
+    return pos;
 }
 
 __device__ __forceinline__ int rank_code(int ped, int base, int win) {
@@ -140,6 +159,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
     __shared__ int s_hist[(NT / 32) * 129];
     __shared__ int s_tmp[144 + 32];
     __shared__ int s_item, s_lo;
+    __shared__ uint32_t s_pnext[32]; // bit q: v_q is an earlier neighbour of v_{i+1} (n1 <= 1024)
     __shared__ unsigned long long s_best;
     constexpr int NW = NT / 32;
 
@@ -149,23 +169,25 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
 
     // per-CTA frontier (two buffers): ped[K], usedT[W][K], mapT[n1max][K]
     uint8_t *scr = a.scratch + (int64_t)blockIdx.x * a.scratch_stride;
-    const int64_t fb = (int64_t)Kc * (4 + 4 * W + a.n1max); // bytes per frontier buffer
+    const int64_t fb = (int64_t)Kc * (4 + 8 * W + a.n1max); // bytes per frontier buffer
     // per-level work arrays: shared memory (SMEM) or, for large K, this CTA's global scratch
     uint8_t *wk = SMEM ? dsmem : scr + 2 * fb;
     int32_t *s_pq = reinterpret_cast<int32_t *>(dsmem + a.sm.pq);
     int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
     uint8_t *s_e2 = dsmem + a.sm.e2;
     uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
-    int32_t *sPed = reinterpret_cast<int32_t *>(wk + a.sm.ped);
-    uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);
-    uint32_t *sB = reinterpret_cast<uint32_t *>(wk + a.sm.b);
+    int32_t *selped = reinterpret_cast<int32_t *>(wk + a.sm.ped); // PED of survivor k (-1: recompute)
+    uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [K][W]
+    int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
     uint8_t *sT = wk + a.sm.t;
     uint8_t *codes = wk + a.sm.codes;
     uint32_t *sel = reinterpret_cast<uint32_t *>(wk + a.sm.sel);
 
     auto fped = [&](int b) { return reinterpret_cast<int32_t *>(scr + b * fb); };
     auto fused = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + 4 * (int64_t)Kc); };
-    auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 4 * W); };
+    // BT[W][K]: B_p of the level about to be expanded, built by the previous level's update
+    auto fbt = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + (int64_t)Kc * (4 + 4 * W)); };
+    auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 8 * W); };
 
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
@@ -174,7 +196,6 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
         if (item >= a.ngroup) return;
         const PairDesc pd = a.descs[a.order[item]];
         const int n1 = pd.n1, n2 = pd.n2, n2p = pd.n2p;
-        const int cs = (n2 + 1 + 3) & ~3;
         const int32_t *vl1 = reinterpret_cast<const int32_t *>(a.blob + pd.vl1);
         const int32_t *vl2 = reinterpret_cast<const int32_t *>(a.blob + pd.vl2);
         const int32_t *pptr = reinterpret_cast<const int32_t *>(a.blob + pd.pptr);
@@ -200,7 +221,10 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
         }
         // root node: lambda empty, all of V2 remaining, PED 0
         if (threadIdx.x == 0) fped(0)[0] = 0;
-        if (threadIdx.x < W) fused(0)[(int64_t)threadIdx.x * Kc] = 0u;
+        if (threadIdx.x < W) {
+            fused(0)[(int64_t)threadIdx.x * Kc] = 0u;
+            fbt(0)[(int64_t)threadIdx.x * Kc] = 0u; // P_0 is empty
+        }
         int N = 1, lo = 0, cur = 0;
         int64_t children = 0, parents = 0, algb = 0;
 
@@ -211,7 +235,19 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             int32_t *Qped = fped(cur ^ 1);
             uint32_t *QusedT = fused(cur ^ 1);
             uint8_t *QmapT = fmap(cur ^ 1);
+            const uint32_t *PBT = fbt(cur);
+            uint32_t *QBT = fbt(cur ^ 1);
             const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
+            // membership of P_{i+1} over q (for the next level's B, built during the update)
+            for (int x = threadIdx.x; x < 32; x += NT) s_pnext[x] = 0u;
+            block_sync();
+            if (i + 1 < n1) {
+                const int nb = __ldg(pptr + i + 1), ne = __ldg(pptr + i + 2);
+                for (int k = nb + threadIdx.x; k < ne; k += NT) {
+                    const int q = __ldg(pq + k);
+                    atomicOr(&s_pnext[q >> 5], 1u << (q & 31));
+                }
+            }
             for (int k = threadIdx.x; k < d; k += NT) {
                 s_pq[k] = __ldg(pq + pbeg + k);
                 s_pl[k] = __ldg(pl + pbeg + k);
@@ -219,72 +255,75 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
             const int vl1i = __ldg(vl1 + i);
             int cv[W];
+            uint32_t Vm[W], Mm[W]; // existing targets / label mismatches, bit u of word u >> 5
 #pragma unroll
-            for (int s = 0; s < W; ++s) cv[s] = (vl2r[s] == vl1i) ? 0 : c.vsub;
+            for (int s = 0; s < W; ++s) {
+                cv[s] = (vl2r[s] == vl1i) ? 0 : c.vsub;
+                Vm[s] = __ballot_sync(FULL, lane + 32 * s < n2);
+                Mm[s] = __ballot_sync(FULL, lane + 32 * s < n2 && vl2r[s] != vl1i);
+            }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
-            block_sync();
+            block_sync(); // P_i list and zeroed histograms visible
 
-            // ---------------- P: parent prepass (coalesced over parents) ----------------
-            for (int p = threadIdx.x; p < N; p += NT) {
-                sPed[p] = Pped[p];
+            // ---------------- P: parents -> used masks in shared memory, compact code offsets ----------------
+            // Parent p has f_p = n2 - |used_p| substitution children + 1 deletion child; its rank codes
+            // occupy codes[off_p, off_p + f_p + 1) in (target ascending, deletion last) = lin order.
+            const int ppt = (N + NT - 1) / NT;
+            const int pb = min(N, threadIdx.x * ppt), pe = min(N, pb + ppt);
+            int nloc = 0;
+            for (int p = pb; p < pe; ++p) {
+                int usedc = 0;
 #pragma unroll
-                for (int w = 0; w < W; ++w) sU[p * W + w] = PusedT[(int64_t)w * Kc + p];
-                if (!LAB) {
-                    uint32_t B[W];
-#pragma unroll
-                    for (int w = 0; w < W; ++w) B[w] = 0u;
-#pragma unroll 4
-                    for (int k = 0; k < d; ++k) {
-                        const int t = PmapT[(int64_t)s_pq[k] * Kc + p];
-#pragma unroll
-                        for (int w = 0; w < W; ++w)
-                            B[w] |= (t != MAP_DEL && (t >> 5) == w) ? (1u << (t & 31)) : 0u;
-                    }
-#pragma unroll
-                    for (int w = 0; w < W; ++w) sB[p * W + w] = B[w];
-                } else {
+                for (int w = 0; w < W; ++w) {
+                    const uint32_t U = PusedT[(int64_t)w * Kc + p];
+                    sU[p * W + w] = U;
+                    usedc += __popc(U);
+                }
+                nloc += n2 - usedc + 1;
+                if (LAB) {
                     const int dd = min(d, DMAX);
                     for (int k = 0; k < dd; ++k) sT[k * Kc + p] = PmapT[(int64_t)s_pq[k] * Kc + p];
                 }
+            }
+            int obase, dummy, ci, dummy2;
+            block_scan2<NT>(nloc, 0, obase, dummy, ci, dummy2, s_tmp); // ci = candidates of the level
+            for (int p = pb; p < pe; ++p) {
+                sOff[p] = obase;
+                int usedc = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) usedc += __popc(sU[p * W + w]);
+                obase += n2 - usedc + 1;
+            }
+            if (threadIdx.x == 0) {
+                sOff[N] = ci;
+                for (int x = ci; x < ((ci + 3) & ~3); ++x) codes[x] = (uint8_t)CODE_INVALID;
             }
             block_sync();
 
             // ---------------- A + T: branch, rank codes, histogram, threshold ----------------
             const int chunk = (N + NW - 1) / NW;
             const int p0 = min(N, warp * chunk), p1 = min(N, p0 + chunk);
-            int base = lo, below = 0, ci = 0, tcode = 256, rq = 0, below_add = 0;
-            bool first = true, keepall = false, retry = false;
-            // exact histogram of rank codes 1..win (win <= 128): one private row per warp, shared atomics
+            int base = lo, below = 0, tcode = 256, rq = 0, below_add = 0;
+            bool keepall = ci <= K, retry = false;
+            // exact histogram of rank codes 1..win (win <= 127): one private row per warp, shared atomics
             int *whist = s_hist + warp * 129;
+            auto hist_add = [&](int code) {
+                if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
+            };
             for (;;) {
-                int wcount = 0;
-                auto hist_add = [&](int code) {
-                    if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
-                };
-                const bool tpp = !LAB && N >= NT / 2;
-                if (tpp) {
+                if (!LAB && N >= NT / 2) {
                     // wide frontier: thread per parent, iterating only the parent's free targets (no idle lanes)
-                    uint32_t Mm[W], Vm[W];
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        Vm[w] = __ballot_sync(FULL, lane + 32 * w < n2);                   // targets that exist
-                        Mm[w] = __ballot_sync(FULL, lane + 32 * w < n2 && vl2r[w] != vl1i); // label mismatches
-                    }
                     for (int p = threadIdx.x; p < N; p += NT) {
-                        const int pedp = sPed[p];
+                        const int pedp = Pped[p];
                         uint32_t U[W], B[W];
 #pragma unroll
-                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = sB[p * W + w]; }
-                        uint8_t *crow = codes + p * cs;
-                        for (int x = 0; x < cs / 4; ++x) reinterpret_cast<uint32_t *>(crow)[x] = 0xffffffffu;
-                        const int cdel = rank_code(pedp + dDel, base, win); // deletion child (PAPER.md:210, C5)
-                        crow[n2] = (uint8_t)cdel;
-                        hist_add(cdel);
-                        int nf = 1;
+                        // B_p: images of the earlier g1 neighbours of v_i (replaces VFrom/VTo)
+                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = PBT[(int64_t)w * Kc + p]; }
+                        uint8_t *crow = codes + sOff[p];
+                        int r = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
                             uint32_t F = Vm[w] & ~U[w];
-                            nf += __popc(F);
                             while (F) {
                                 const int bt = __ffs(F) - 1;
                                 F &= F - 1;
@@ -292,94 +331,90 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                                 int cnt = 0, cb = 0;
 #pragma unroll
                                 for (int x = 0; x < W; ++x) {
-                                    const uint32_t r = sAdj[u * W + x];
-                                    cnt += __popc(r & U[x]);
-                                    cb += __popc(r & B[x]);
+                                    const uint32_t rw = sAdj[u * W + x];
+                                    cnt += __popc(rw & U[x]);
+                                    cb += __popc(rw & B[x]);
                                 }
                                 const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb;
                                 const int code = rank_code(ped, base, win);
-                                crow[u] = (uint8_t)code;
+                                crow[r++] = (uint8_t)code;
                                 hist_add(code);
                             }
                         }
-                        wcount += nf;
+                        const int cdel = rank_code(pedp + dDel, base, win); // deletion child (PAPER.md:210, C5)
+                        crow[r] = (uint8_t)cdel;
+                        hist_add(cdel);
                     }
-                    wcount = __reduce_add_sync(FULL, wcount);
-                } else
-                for (int p = p0; p < p1; ++p) {
-                    const int pedp = sPed[p];
-                    uint32_t U[W];
-                    int usedc = 0;
+                } else {
+                    // narrow frontier (or labelled edges): warp per parent, lane l owns targets l + 32 s
+                    for (int p = p0; p < p1; ++p) {
+                        const int pedp = Pped[p];
+                        uint32_t U[W];
 #pragma unroll
-                    for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; usedc += __popc(U[w]); }
-                    int ped_s[W];
-                    if (!LAB) {
-                        uint32_t B[W];
+                        for (int w = 0; w < W; ++w) U[w] = sU[p * W + w];
+                        int ped_s[W];
+                        if (!LAB) {
+                            uint32_t B[W];
 #pragma unroll
-                        for (int w = 0; w < W; ++w) B[w] = sB[p * W + w];
-#pragma unroll
-                        for (int s = 0; s < W; ++s) {
-                            int cnt = 0, cb = 0;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) {
-                                cnt += __popc(A[s][w] & U[w]);
-                                cb += __popc(A[s][w] & B[w]);
-                            }
-                            ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb;
-                        }
-                    } else {
-                        int cb[W], mis[W];
-#pragma unroll
-                        for (int s = 0; s < W; ++s) { cb[s] = 0; mis[s] = 0; }
-                        for (int k = 0; k < d; ++k) {
-                            const int tt = (k < DMAX) ? sT[k * Kc + p] : PmapT[(int64_t)s_pq[k] * Kc + p];
-                            if (tt == MAP_DEL) continue;
-                            const int ll = s_pl[k];
-                            const uint8_t *row = s_e2 + tt * n2p;
+                            for (int w = 0; w < W; ++w) B[w] = PBT[(int64_t)w * Kc + p];
 #pragma unroll
                             for (int s = 0; s < W; ++s) {
-                                const int u = lane + 32 * s;
-                                const int e = (u < n2p) ? row[u] : 0;
-                                cb[s] += (e != 0);
-                                mis[s] += (e != 0) & (e != ll);
+                                int cnt = 0, cb = 0;
+#pragma unroll
+                                for (int w = 0; w < W; ++w) {
+                                    cnt += __popc(A[s][w] & U[w]);
+                                    cb += __popc(A[s][w] & B[w]);
+                                }
+                                ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb;
+                            }
+                        } else {
+                            int cb[W], mis[W];
+#pragma unroll
+                            for (int s = 0; s < W; ++s) { cb[s] = 0; mis[s] = 0; }
+                            for (int k = 0; k < d; ++k) {
+                                const int tt = (k < DMAX) ? sT[k * Kc + p] : PmapT[(int64_t)s_pq[k] * Kc + p];
+                                if (tt == MAP_DEL) continue;
+                                const int ll = s_pl[k];
+                                const uint8_t *row = s_e2 + tt * n2p;
+#pragma unroll
+                                for (int s = 0; s < W; ++s) {
+                                    const int u = lane + 32 * s;
+                                    const int e = (u < n2p) ? row[u] : 0;
+                                    cb[s] += (e != 0);
+                                    mis[s] += (e != 0) & (e != ll);
+                                }
+                            }
+#pragma unroll
+                            for (int s = 0; s < W; ++s) {
+                                int cnt = 0;
+#pragma unroll
+                                for (int w = 0; w < W; ++w) cnt += __popc(A[s][w] & U[w]);
+                                ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb[s] + c.esub * mis[s];
                             }
                         }
+                        uint8_t *crow = codes + sOff[p];
+                        int r = 0;
+                        const unsigned lmask = lanemask_lt();
 #pragma unroll
                         for (int s = 0; s < W; ++s) {
-                            int cnt = 0;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) cnt += __popc(A[s][w] & U[w]);
-                            ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb[s] + c.esub * mis[s];
+                            const int u = lane + 32 * s;
+                            const bool sub = (u < n2) && !((U[s] >> lane) & 1u);
+                            const unsigned bal = __ballot_sync(FULL, sub);
+                            const int code = sub ? rank_code(ped_s[s], base, win) : CODE_INVALID;
+                            if (sub) crow[r + __popc(bal & lmask)] = (uint8_t)code;
+                            hist_add(code);
+                            r += __popc(bal);
                         }
+                        if (lane == 0) {
+                            const int cdel = rank_code(pedp + dDel, base, win);
+                            crow[r] = (uint8_t)cdel;
+                            hist_add(cdel);
+                        }
+                        __syncwarp();
                     }
-                    const int pedD = pedp + dDel;
-                    uint8_t *crow = codes + p * cs;
-#pragma unroll
-                    for (int s = 0; s < W; ++s) {
-                        const int u = lane + 32 * s;
-                        const bool sub = (u < n2) && !((U[s] >> lane) & 1u);
-                        const bool del = (u == n2);
-                        int code = CODE_INVALID;
-                        if (sub || del) code = rank_code(sub ? ped_s[s] : pedD, base, win);
-                        hist_add(code);
-                        if (u < cs) crow[u] = (uint8_t)code;
-                    }
-                    if (32 * W < cs) { // n2 == 32 W: the deletion slot lies past the lane slots
-                        const int u = 32 * W + lane;
-                        const int code = (u == n2) ? rank_code(pedD, base, win) : CODE_INVALID;
-                        hist_add(code);
-                        if (u < cs) crow[u] = (uint8_t)code;
-                    }
-                    wcount += n2 - usedc + 1; // |R_V2| substitutions + the deletion (C5)
                 }
-                if (first && lane == 0) s_tmp[144 + warp] = wcount; // (block_scan2 owns s_tmp[0..130))
                 block_sync();
                 { // T: every warp derives the same threshold from the per-warp histograms (4 codes per lane)
-                    if (first) {
-                        ci = lane < NW ? s_tmp[144 + lane] : 0;
-                        ci = __reduce_add_sync(FULL, ci);
-                    }
-                    keepall = ci <= K;
                     int hv[4], sum = 0;
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
@@ -397,14 +432,11 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         if (lane >= o) incl += y;
                     }
                     const unsigned hm = __ballot_sync(FULL, !keepall && (below + incl >= K));
-                    const int total = __shfl_sync(FULL, incl, 31);
+                    below_add = __shfl_sync(FULL, incl, 31);
                     retry = !keepall && hm == 0u;
-                    int tc = 0, rr = 0;
                     if (hm) {
                         const int L = __ffs(hm) - 1;
-                        int cum = below + incl - sum;
-                        int c2 = cum;
-                        tc = 0;
+                        int c2 = below + incl - sum, tc = 0, rr = 0;
 #pragma unroll
                         for (int x = 0; x < 4; ++x) {
                             if (tc == 0 && c2 + hv[x] >= K) { tc = 4 * lane + 1 + x; rr = K - c2; }
@@ -413,23 +445,21 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         tcode = __shfl_sync(FULL, tc, L);
                         rq = __shfl_sync(FULL, rr, L);
                     }
-                    below_add = total;
                 }
                 if (!retry) break; // (uniform: every warp computed the same value)
                 // the K-th smallest PED lies beyond the window: slide it (all codes < base are kept)
                 block_sync(); // all warps have read the histograms
                 below += below_add;
                 base += win;
-                first = false;
                 for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
                 block_sync();
             }
 
-            // ---------------- S: exact threshold + selection by segment scan over the code words ----------------
+            // ---------------- S: selection by segment scan over the compact code words ----------------
             int Nn;
             {
                 const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes);
-                const int nwords = N * cs / 4;
+                const int nwords = (ci + 3) >> 2;
                 const int seg = (nwords + NT - 1) / NT;
                 const int w0 = min(nwords, threadIdx.x * seg), w1 = min(nwords, w0 + seg);
                 if (keepall) { tcode = 256; rq = 0; }
@@ -453,9 +483,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                 Nn = keepall ? lttot : K;
                 int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
                 if (lt + eq > 0) {
-                    int pc = (4 * w0) / cs, uc = 4 * w0 - pc * cs;
-                    for (int x = w0; x < w1; ++x, uc += 4) {
-                        if (uc >= cs) { uc -= cs; ++pc; }
+                    for (int x = w0; x < w1; ++x) {
                         const uint32_t v = cw[x];
                         uint32_t mlt, meq = 0u;
                         if (keepall) mlt = valid(v);
@@ -466,11 +494,15 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         }
                         uint32_t m = mlt | meq;
                         while (m) {
-                            const int bit = __ffs(m) - 1, b = bit >> 3;
+                            const int bit = __ffs(m) - 1;
                             m &= m - 1;
                             bool keep = (mlt >> bit) & 1u;
                             if (!keep) { keep = eq_seen < rq; eq_seen++; }
-                            if (keep) sel[out++] = ((uint32_t)pc << 8) | (uint32_t)(uc + b);
+                            if (!keep) continue;
+                            const int code = (int)((v >> (bit & ~7)) & 0xffu);
+                            sel[out] = (uint32_t)(4 * x + (bit >> 3)); // compact code index; decoded below
+                            selped[out] = (code >= 1 && code <= win) ? base + code - 1 : -1;
+                            ++out;
                         }
                     }
                 }
@@ -485,33 +517,55 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             }
             block_sync();
 
+            // ---------------- decode survivors: compact code index -> (parent p, child j) ----------------
+            for (int k = threadIdx.x; k < Nn; k += NT) {
+                const int cidx = (int)sel[k];
+                int plo = 0, phi = N - 1; // last p with off_p <= cidx
+                while (plo < phi) {
+                    const int mid = (plo + phi + 1) >> 1;
+                    if (sOff[mid] <= cidx) plo = mid; else phi = mid - 1;
+                }
+                const int rnk = cidx - sOff[plo], f = sOff[plo + 1] - sOff[plo] - 1;
+                int j = n2;
+                if (rnk < f) { // the rnk-th free target of parent plo
+                    int rr = rnk;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        const uint32_t F = Vm[w] & ~sU[plo * W + w];
+                        const int cnt = __popc(F);
+                        if (rr >= 0 && rr < cnt) j = 32 * w + select_bit(F, rr);
+                        rr -= cnt;
+                    }
+                }
+                sel[k] = ((uint32_t)plo << 8) | (uint32_t)j;
+            }
+            block_sync();
+
             // ---------------- U: write the next frontier (coalesced over k) ----------------
             for (int k = threadIdx.x; k < Nn; k += NT) {
-                const uint32_t v = sel[k];
-                const int p = (int)(v >> 8), j = (int)(v & 255u);
-                const int code = codes[p * cs + j];
-                int ped;
-                if (code >= 1 && code <= win) ped = base + code - 1;
-                else { // saturated rank code: recompute the child's PED (rare)
-                    const int pedp = sPed[p];
+                int ped = selped[k];
+                if (ped < 0) { // saturated rank code: recompute the child's PED (rare)
+                    const uint32_t v = sel[k];
+                    const int p = (int)(v >> 8), j = (int)(v & 255u);
+                    const int pedp = Pped[p];
                     if (j == n2) ped = pedp + dDel;
                     else {
                         int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
-                        for (int w = 0; w < W; ++w) cnt += __popc(__ldg(adj2 + j * W + w) & sU[p * W + w]);
+                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & sU[p * W + w]);
                         if (!LAB) {
 #pragma unroll
-                            for (int w = 0; w < W; ++w) cb += __popc(__ldg(adj2 + j * W + w) & sB[p * W + w]);
+                            for (int w = 0; w < W; ++w) cb += __popc(sAdj[j * W + w] & PBT[(int64_t)w * Kc + p]);
                         } else {
                             for (int q = 0; q < d; ++q) {
-                                const int t = (q < DMAX) ? sT[q * Kc + p] : PmapT[(int64_t)s_pq[q] * Kc + p];
+                                const int t = PmapT[(int64_t)s_pq[q] * Kc + p];
                                 if (t == MAP_DEL) continue;
                                 const int e = s_e2[t * n2p + j];
                                 cb += (e != 0);
                                 mis += (e != 0) & (e != s_pl[q]);
                             }
                         }
-                        ped = pedp + ((__ldg(vl2 + j) == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - ee * cb + c.esub * mis;
+                        ped = pedp + ((vl2[j] == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - ee * cb + c.esub * mis;
                     }
                 }
                 Qped[k] = ped;
@@ -525,10 +579,11 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             }
             {
                 const int nk4 = (Nn + 3) >> 2;
+                const bool inext = (i + 1 < n1) && ((s_pnext[i >> 5] >> (i & 31)) & 1u);
                 for (int x = threadIdx.x; x < nk4; x += NT) {
                     const int k0 = 4 * x;
                     int pp[4];
-                    uint32_t last = 0;
+                    uint32_t last = 0, Bn[4][W];
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
                         const int k = min(k0 + b, Nn - 1);
@@ -536,6 +591,9 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         pp[b] = (int)(v >> 8);
                         const int j = (int)(v & 255u);
                         last |= ((j == n2) ? (uint32_t)MAP_DEL : (uint32_t)j) << (8 * b);
+#pragma unroll
+                        for (int w = 0; w < W; ++w)
+                            Bn[b][w] = (inext && j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u;
                     }
 #pragma unroll 4
                     for (int q = 0; q < i; ++q) {
@@ -543,8 +601,21 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         const uint32_t word = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |
                                               ((uint32_t)row[pp[2]] << 16) | ((uint32_t)row[pp[3]] << 24);
                         *reinterpret_cast<uint32_t *>(QmapT + (int64_t)q * Kc + k0) = word;
+                        if ((s_pnext[q >> 5] >> (q & 31)) & 1u) { // v_q is an earlier neighbour of v_{i+1}
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const uint32_t t = (word >> (8 * b)) & 0xffu;
+#pragma unroll
+                                for (int w = 0; w < W; ++w)
+                                    Bn[b][w] |= (t != (uint32_t)MAP_DEL && (int)(t >> 5) == w) ? (1u << (t & 31)) : 0u;
+                            }
+                        }
                     }
                     *reinterpret_cast<uint32_t *>(QmapT + (int64_t)i * Kc + k0) = last;
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) QBT[(int64_t)w * Kc + k0 + b] = Bn[b][w];
                 }
             }
             children += ci;

@@ -180,7 +180,7 @@ void check_overflow(const fastged_graph_t *g1, const fastged_graph_t *g2, const 
 
 // Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024, K <= 2^24.
 bool fits_batched(const fastged_graph_t *g1, const fastged_graph_t *g2, int64_t k) {
-    return g2->n <= 128 && g1->n <= 1024 && k <= (1 << 24);
+    return g2->n <= 128 && g1->n <= 1024 && k <= (1 << 24); // (n1 <= 1024: P_{i+1} membership bitmask)
 }
 
 // ---------------------------------------------------------------- packing
@@ -478,9 +478,9 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         // per-level work arrays
         size_t wk = 0;
         auto put = [&](int32_t &field, size_t bytes) { field = (int)wk; wk += align16(bytes); };
-        put(a.sm.ped, 4 * Kc);
-        put(a.sm.u, 4 * Kc * W);
-        put(a.sm.b, 4 * Kc * W);
+        put(a.sm.ped, 4 * Kc);             // survivor PEDs
+        put(a.sm.u, 4 * Kc * W);           // parent used masks
+        put(a.sm.b, 4 * (Kc + 1));         // compact code offsets
         put(a.sm.t, key.lab ? (size_t)fg::DMAX * Kc : 0);
         put(a.sm.codes, Kc * a.csmax);
         put(a.sm.sel, 4 * Kc);
@@ -491,7 +491,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             smem += wk;
         }
         a.sm.bytes = (int)smem;
-        size_t per_cta = 2 * Kc * (4 + 4 * (size_t)W + a.n1max) + (in_smem ? 0 : wk);
+        size_t per_cta = 2 * Kc * (4 + 8 * (size_t)W + a.n1max) + (in_smem ? 0 : wk);
         per_cta = (per_cta + 255) & ~(size_t)255;
         void *kern = batch_kernel_for(W, key.lab, in_smem);
         if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);

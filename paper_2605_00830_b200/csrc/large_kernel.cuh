@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             for (int k = threadIdx.x; k < 256; k += blockDim.x)
                 if (s_hist[k]) atomicAdd(&gh[k], s_hist[k]);
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
-            __syncwarp();
+            block_sync();
         grid.sync();
             // T: every CTA derives the same threshold
             const int64_t ci = a.ci[i];
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             eq = __reduce_add_sync(FULL, eq);
             if (lane == 0) { a.wlt[gw] = lt; a.weq[gw] = eq; }
         }
-        __syncwarp();
+        block_sync();
         grid.sync();
 
         // ---------------- prefix for this CTA's warps (computed redundantly per CTA) ----------------
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             a.levels_out[3 * i + 1] = a.ci[i];
             a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
         }
-        __syncwarp();
+        block_sync();
         grid.sync();
 
         // ---------------- C2: next frontier ----------------
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         }
         parents += N;
         algb += (int64_t)N * (4 + (int)sizeof(MapT) * d) + (int64_t)Nn * ((int)sizeof(MapT) * (2 * i + 1) + 8);
-        __syncwarp();
+        block_sync();
         grid.sync();
         N = Nn;
         lo = a.lo[i + 1];
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
                 atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)k);
             }
         }
-        __syncwarp();
+        block_sync();
         grid.sync();
         if (blockIdx.x == 0) {
             const unsigned long long best = *a.best;
