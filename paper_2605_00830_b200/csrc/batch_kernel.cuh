@@ -595,19 +595,32 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         for (int w = 0; w < W; ++w)
                             Bn[b][w] = (inext && j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u;
                     }
-#pragma unroll 4
-                    for (int q = 0; q < i; ++q) {
-                        const uint8_t *row = PmapT + (int64_t)q * Kc;
-                        const uint32_t word = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |
-                                              ((uint32_t)row[pp[2]] << 16) | ((uint32_t)row[pp[3]] << 24);
-                        *reinterpret_cast<uint32_t *>(QmapT + (int64_t)q * Kc + k0) = word;
-                        if ((s_pnext[q >> 5] >> (q & 31)) & 1u) { // v_q is an earlier neighbour of v_{i+1}
+                    // lambda columns 0..i-1: gather 8 columns x 4 survivors into registers, then store
+                    // (loads of a chunk are issued together; QmapT/PmapT are distinct buffers)
+                    for (int q0 = 0; q0 < i; q0 += 8) {
+                        uint32_t wd[8];
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) {
-                                const uint32_t t = (word >> (8 * b)) & 0xffu;
+                        for (int z = 0; z < 8; ++z) {
+                            const int q = min(q0 + z, i - 1);
+                            const uint8_t *row = PmapT + (int64_t)q * Kc;
+                            // plain loads: this CTA wrote the column in the previous level (visible after the
+                            // barrier); the read-only (.nc) path is not coherent with such writes
+                            wd[z] = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |
+                                    ((uint32_t)row[pp[2]] << 16) | ((uint32_t)row[pp[3]] << 24);
+                        }
 #pragma unroll
-                                for (int w = 0; w < W; ++w)
-                                    Bn[b][w] |= (t != (uint32_t)MAP_DEL && (int)(t >> 5) == w) ? (1u << (t & 31)) : 0u;
+                        for (int z = 0; z < 8; ++z) {
+                            const int q = q0 + z;
+                            if (q >= i) break;
+                            *reinterpret_cast<uint32_t *>(QmapT + (int64_t)q * Kc + k0) = wd[z];
+                            if ((s_pnext[q >> 5] >> (q & 31)) & 1u) { // v_q is an earlier neighbour of v_{i+1}
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    const uint32_t t = (wd[z] >> (8 * b)) & 0xffu;
+#pragma unroll
+                                    for (int w = 0; w < W; ++w)
+                                        Bn[b][w] |= (t != (uint32_t)MAP_DEL && (int)(t >> 5) == w) ? (1u << (t & 31)) : 0u;
+                                }
                             }
                         }
                     }
