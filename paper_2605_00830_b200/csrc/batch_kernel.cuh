@@ -1,31 +1,34 @@
 // batch_kernel.cuh -- the batched K-Best search: one CTA runs one (g1, g2) pair through all
 // levels of Alg. 1 and then takes the next pair from a work counter.
 //
-// Frontier (per CTA, global scratch, structure-of-arrays so every per-level pass is coalesced):
-//   ped[K] int32, usedT[W][K] uint32 (bit u = g2 vertex u used), mapT[n1][K] uint8 (lambda,
-//   255 = deleted).  Column k of usedT/mapT is frontier node k.
+// Frontier (per CTA, global scratch, structure of arrays so every per-level pass is coalesced):
+//   ped[K] int32, usedT[W][K] uint32 (bit u = g2 vertex u used), BT[W][K] uint32 (B_p of the next
+//   level, see U), mapT[n1][K] uint8 (lambda, 255 = deleted).  Column k is frontier node k.
 //
 // Per level i (g1 vertex v_i, reading C4):
-//   P  Parent prepass (thread per parent): PED, used mask and B_p -- the images of the earlier
-//      g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors) -- are staged
-//      in shared memory; the lambda gathers are coalesced across parents (transposed layout).
-//   A  Branch (Alg. 2).  A warp takes one parent at a time;
-//      lane l owns the g2 vertices u = l + 32 s (s < W), whose bit-packed adjacency rows stay in
-//      registers for the whole pair.  The child PED is the paper's incremental evaluation
-//      PED = E(parent) + c(v<-u) + Imp_cost with the three implied-edge cases of PAPER.md:103-116
-//      regrouped into popcounts:
+//   P  Parents' used masks to shared memory; parent p owns the compact code range
+//      [off_p, off_p + f_p + 1): its f_p free targets in ascending order, then its deletion child
+//      (= the (parent, child) lin order of reading C12/C13); off_p from a block scan.
+//   A  Branch (Alg. 2).  The child PED is the paper's incremental
+//      evaluation PED = E(parent) + c(v<-u) + Imp_cost with the three implied-edge cases of
+//      PAPER.md:103-116 regrouped into popcounts:
 //          Delta(u)   = cv(i,u) + edel*d_i + eins*cnt_p(u) - (edel+eins)*cB_p(u) + esub*mis_p(u)
 //          Delta(DEL) = vdel + edel*d_i
-//      cnt_p(u) = popc(adj2[u] & used_p), cB_p(u) = popc(adj2[u] & B_p).  Each child is written as
-//      a one-byte rank code (PED - base + 1, saturated) to shared memory and counted in a 256-bin
-//      shared histogram (warp-aggregated with match.any).  Children never reach HBM.
-//   T  Threshold (replaces the paper's local/global ranking): a warp scan of the
-//      histogram gives the threshold PED t and the quota r of ties at t; exactly min(K, c_i)
-//      children are kept, the smallest under (PED, parent, child) (reading C12).  No sort.
-//   S  Selection: every thread owns a contiguous run of code words; SIMD byte compares count
-//      codes < t / == t, a block scan gives each thread its output offset and tie admissions,
-//      and survivors are written in (parent, child) order (C13).
-//   U  Update: the next frontier columns are written with coalesced stores.
+//      cnt_p(u) = popc(adj2[u] & used_p), cB_p(u) = popc(adj2[u] & B_p), B_p = images of the earlier
+//      g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors); labelled edges
+//      compare the edge labels of (u, t_k) per earlier neighbour (mis_p).  Wide frontiers: a thread
+//      per parent iterates only that parent's free targets; narrow ones: a warp per parent with
+//      lane-owned targets.  Each child becomes a one-byte rank code (PED - base + 1, saturated) in
+//      shared memory and one atomic in its warp's private 128-bin histogram.  Children never reach HBM.
+//   T  Threshold (replaces the paper's local/global ranking): every warp scans the
+//      histograms and derives the same threshold PED t and quota r of ties at t; exactly
+//      min(K, c_i) children are kept, the smallest under (PED, parent, child) (reading C12).  No sort.
+//      If the K-th smallest lies beyond the window the window slides and A is repeated.
+//   S  Selection: every thread owns a contiguous run of code words; SWAR byte compares count codes
+//      < t / == t, a block scan gives each thread its output offset and tie admissions, survivors'
+//      code indices are written in (parent, child) order (C13), then decoded to (p, j) balanced.
+//   U  Update: next frontier columns with coalesced stores; while copying the
+//      lambda columns, B_p of the next level is accumulated (no separate gathers).
 // After the last level each survivor gets the insertion completion (C6) and the
 // argmin by (total, position) is written out (C10).
 #pragma once
@@ -311,14 +314,17 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                 if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
             };
             for (;;) {
-                if (!LAB && N >= NT / 2) {
+                if (N >= NT / 2 && (!LAB || d <= DMAX)) {
                     // wide frontier: thread per parent, iterating only the parent's free targets (no idle lanes)
                     for (int p = threadIdx.x; p < N; p += NT) {
                         const int pedp = Pped[p];
                         uint32_t U[W], B[W];
-#pragma unroll
                         // B_p: images of the earlier g1 neighbours of v_i (replaces VFrom/VTo)
-                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = PBT[(int64_t)w * Kc + p]; }
+#pragma unroll
+                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = LAB ? 0u : PBT[(int64_t)w * Kc + p]; }
+                        int tl[DMAX]; // labelled edges: the images t_k themselves (d <= DMAX)
+#pragma unroll
+                        for (int k = 0; k < DMAX; ++k) tl[k] = (LAB && k < d) ? (int)sT[k * Kc + p] : MAP_DEL;
                         uint8_t *crow = codes + sOff[p];
                         int r = 0;
 #pragma unroll
@@ -328,14 +334,23 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                                 const int bt = __ffs(F) - 1;
                                 F &= F - 1;
                                 const int u = 32 * w + bt;
-                                int cnt = 0, cb = 0;
+                                int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
                                 for (int x = 0; x < W; ++x) {
                                     const uint32_t rw = sAdj[u * W + x];
                                     cnt += __popc(rw & U[x]);
-                                    cb += __popc(rw & B[x]);
+                                    if (!LAB) cb += __popc(rw & B[x]);
                                 }
-                                const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb;
+                                if (LAB) { // edge label of (u, t_k) vs the g1 edge label (v_i, v_q_k)
+#pragma unroll
+                                    for (int k = 0; k < DMAX; ++k) {
+                                        if (tl[k] == MAP_DEL) continue;
+                                        const int e = s_e2[tl[k] * n2p + u];
+                                        cb += (e != 0);
+                                        mis += (e != 0) & (e != s_pl[k]);
+                                    }
+                                }
+                                const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb + c.esub * mis;
                                 const int code = rank_code(ped, base, win);
                                 crow[r++] = (uint8_t)code;
                                 hist_add(code);
