@@ -52,6 +52,8 @@ extern "C" {
 #define FASTGED_FLAG_TIMING 1u      /* record CUDA events around every kernel launch (fastged_get_stats) */
 #define FASTGED_FLAG_DEBUG_WINDOW 2u /* test only: 2-wide rank window, forces the multi-pass rank path   */
 #define FASTGED_FLAG_FORCE_LARGE 4u  /* test only: solve_pair uses the whole-GPU path even for small pairs */
+#define FASTGED_FLAG_VIRTUAL_SHARDS 8u /* test only: world_size shards of one pair on this handle's GPU,
+                                         exchanged by device copies instead of NCCL (rank, nccl_id ignored) */
 
 /* Limits of this build (exceeding one returns FASTGED_ERR_CAPACITY, never a silent change). */
 #define FASTGED_MAX_N 65534        /* vertices of a source graph g1                               */
@@ -175,6 +177,10 @@ void fastged_batch_free(fastged_handle_t *h, fastged_batch_t *b);
 
 /* Counters of the last solve/run call. */
 int fastged_get_stats(const fastged_handle_t *h, fastged_stats_t *out);
+
+/* Writes a new 128-byte ncclUniqueId to out (call on rank 0, broadcast the bytes to every rank, pass
+ * them as fastged_config_t.nccl_id).  FASTGED_ERR_NCCL on failure. */
+int fastged_nccl_unique_id(uint8_t *out);
 
 /* Library version string, e.g. "fastged-b200 0.1 sm_100a". */
 const char *fastged_version(void);

@@ -19,12 +19,13 @@ OK, ERR_ARG, ERR_INPUT, ERR_CAPACITY, ERR_OVERFLOW, ERR_CUDA, ERR_NCCL = range(7
 FLAG_TIMING = 1
 FLAG_DEBUG_WINDOW = 2
 FLAG_FORCE_LARGE = 4
+FLAG_VIRTUAL_SHARDS = 8
 
 # The symbols include/fastged.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fastged_create", "fastged_destroy", "fastged_last_error", "fastged_solve_pair", "fastged_solve_pair_ex",
     "fastged_solve_batch", "fastged_batch_upload", "fastged_batch_run", "fastged_batch_download",
-    "fastged_batch_free", "fastged_get_stats", "fastged_version",
+    "fastged_batch_free", "fastged_get_stats", "fastged_version", "fastged_nccl_unique_id",
 )
 
 
@@ -95,6 +96,8 @@ def lib(path: Optional[str] = None):
     L.fastged_batch_free.restype = None
     L.fastged_get_stats.argtypes = [P, C.POINTER(StatsT)]
     L.fastged_version.restype = C.c_char_p
+    L.fastged_nccl_unique_id.argtypes = [P]
+    L.fastged_nccl_unique_id.restype = C.c_int
     for name in ("fastged_create", "fastged_solve_pair", "fastged_solve_pair_ex", "fastged_solve_batch",
                  "fastged_batch_upload", "fastged_batch_run", "fastged_batch_download", "fastged_get_stats"):
         getattr(L, name).restype = C.c_int
@@ -252,6 +255,15 @@ class DeviceBatch:
             self.free()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for the sharded single-pair mode (rank 0 creates, torch.distributed broadcasts)."""
+    buf = C.create_string_buffer(128)
+    rc = lib().fastged_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc != OK:
+        raise FastGedError(rc, "ncclGetUniqueId failed")
+    return buf.raw
 
 
 def version() -> str:

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfastged.so")
 SRCS = [os.path.join(HERE, "csrc", "fastged.cu")]
-DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "large_kernel.cuh")] + \
+DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "large_kernel.cuh", "shard_kernels.cuh",
+                                                       "shard_host.inc")] + \
     [os.path.join(ROOT, "include", "fastged.h")]
 
 NVCC_FLAGS = [
@@ -17,6 +18,15 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-O2,-Wall,-fopenmp", "-Xptxas", "-v", "-shared",
 ]
+
+
+def nccl_dir() -> str:
+    """NCCL headers/library shipped with the torch wheels (nvidia-nccl-cu12)."""
+    try:
+        import nvidia.nccl
+        return os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+    except Exception:
+        return "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
 
 
 def nvcc() -> str:
@@ -37,7 +47,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SRCS, "-lcudart", "-lgomp"]
+    nd = nccl_dir()
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-o", tmp, *SRCS,
+           "-lcudart", "-lgomp", "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "csrc", "ptxas.log")
     with open(log, "w") as f:

@@ -5,6 +5,7 @@
 // neighbours, labels), copy it to HBM once ("transferred once"), launch the search
 // kernels, copy results back once.  Nothing of the search runs on the host.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -18,6 +19,7 @@
 #include "../../include/fastged.h"
 #include "batch_kernel.cuh"
 #include "large_kernel.cuh"
+#include "shard_kernels.cuh"
 
 namespace {
 
@@ -134,6 +136,7 @@ struct fastged_handle {
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     DevBuf lblob, lbuf; // large single-pair mode
     fastged_batch *tmp = nullptr; // reused by solve_batch / solve_pair
+    ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1, NCCL transport)
 };
 
 namespace {
@@ -708,12 +711,23 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     out->device_ms = ms;
 }
 
+#include "shard_host.inc"
+
 } // namespace
 
 // ================================================================ C ABI
 extern "C" {
 
 const char *fastged_version(void) { return "fastged-b200 0.1 sm_100a"; }
+
+int fastged_nccl_unique_id(uint8_t *out) {
+    if (!out) return FASTGED_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return FASTGED_ERR_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out, &id, sizeof id);
+    return FASTGED_OK;
+}
 
 int fastged_create(const fastged_config_t *cfg, fastged_handle_t **out) {
     g_create_error.clear();
@@ -748,8 +762,13 @@ int fastged_create(const fastged_config_t *cfg, fastged_handle_t **out) {
         }
         CK(cudaEventCreate(&h->ev_begin));
         CK(cudaEventCreate(&h->ev_end));
-        if (h->world > 1)
-            fail(FASTGED_ERR_ARG, "world_size > 1 (sharded single-pair mode) is not available in this build");
+        if (h->world > 1 && !(h->flags & FASTGED_FLAG_VIRTUAL_SHARDS)) {
+            if (!cfg->nccl_id) fail(FASTGED_ERR_ARG, "world_size > 1 needs nccl_id (from fastged_nccl_unique_id on rank 0)");
+            ncclUniqueId id;
+            memcpy(&id, cfg->nccl_id, sizeof id);
+            ncclResult_t nr = ncclCommInitRank(&h->comm, h->world, id, h->rank);
+            if (nr != ncclSuccess) fail(FASTGED_ERR_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(nr));
+        }
         *out = h;
         return FASTGED_OK;
     } catch (const FgError &e) {
@@ -767,6 +786,7 @@ void fastged_destroy(fastged_handle_t *h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm) ncclCommDestroy(h->comm);
     h->lblob.release();
     h->lbuf.release();
     free_batch(h->tmp);
@@ -876,6 +896,10 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
         validate_graph(g2, 0, "g2");
         check_overflow(g1, g2, c, 0);
         if (g1->n > 0 && !out->mapping) fail(FASTGED_ERR_ARG, "out->mapping is NULL");
+        if (h->world > 1) {
+            solve_sharded(h, g1, g2, c, k, out, levels_out);
+            return FASTGED_OK;
+        }
         if (!fits_batched(g1, g2, k) || (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;

@@ -1,0 +1,77 @@
+"""Multi-GPU plumbing (torch.distributed only; every search step runs in libfastged's kernels).
+
+Two modes:
+
+* Batches of independent pairs: pair k goes to rank k mod world (``shard_pairs``); each rank runs
+  ``fastged_solve_batch`` on its own GPU with no data-path collective; ``gather_results`` brings
+  the per-rank results back to rank 0 in global pair order.
+* One large pair: ``sharded_handle`` creates a handle whose frontier is split by parent across
+  all ranks; rank 0 creates the 128-byte ncclUniqueId (``binding.nccl_unique_id``) and
+  torch.distributed broadcasts it; every rank then calls ``solve_pair`` collectively.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+
+def shard_pairs(npairs: int, rank: int, world: int) -> np.ndarray:
+    """Strided assignment: pair k -> rank k mod world (deterministic, balanced by construction)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return np.arange(rank, npairs, world, dtype=np.int64)
+
+
+def broadcast_bytes(payload: Optional[bytes], src: int = 0, group=None) -> bytes:
+    """Broadcast a small byte string from `src` (uses the process group's default device)."""
+    import torch
+    import torch.distributed as dist
+    obj = [payload]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
+def nccl_id_for_group(group=None) -> bytes:
+    """Rank 0 creates the ncclUniqueId; all ranks receive the same 128 bytes."""
+    import torch.distributed as dist
+    from . import binding
+    payload = binding.nccl_unique_id() if dist.get_rank(group) == 0 else None
+    uid = broadcast_bytes(payload, src=0, group=group)
+    assert isinstance(uid, (bytes, bytearray)) and len(uid) == 128
+    return bytes(uid)
+
+
+def sharded_handle(device: int, group=None, flags: int = 0):
+    """A handle for the sharded single-pair mode over all ranks of `group`."""
+    import torch.distributed as dist
+    from . import binding
+    uid = nccl_id_for_group(group)
+    return binding.Handle(device, world_size=dist.get_world_size(group), rank=dist.get_rank(group),
+                          nccl_id=uid, flags=flags)
+
+
+def gather_results(npairs: int, idx: np.ndarray, costs: np.ndarray, maps: np.ndarray, offs: np.ndarray,
+                   n1_all: Sequence[int], group=None) -> Optional[Tuple[np.ndarray, List[np.ndarray]]]:
+    """Collect (cost, mapping) of every pair on rank 0 in global pair order (None on other ranks).
+
+    idx: the global pair indices this rank solved; costs/maps/offs: its solve_batch outputs.
+    """
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = (np.asarray(idx, np.int64), np.asarray(costs, np.int64), np.asarray(maps, np.int32),
+            np.asarray(offs, np.int64))
+    parts = [None] * world if rank == 0 else None
+    dist.gather_object(mine, parts, dst=0, group=group)
+    if rank != 0:
+        return None
+    out_c = np.full(npairs, -1, np.int64)
+    out_m: List[np.ndarray] = [np.zeros(0, np.int32)] * npairs
+    for pidx, pc, pm, po in parts:
+        for x, k in enumerate(pidx):
+            out_c[k] = pc[x]
+            out_m[k] = pm[po[x]:po[x + 1]].copy()
+    assert (out_c >= 0).all(), "a pair was not solved by any rank"
+    for k in range(npairs):
+        assert out_m[k].shape[0] == n1_all[k]
+    return out_c, out_m

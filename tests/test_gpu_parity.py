@@ -269,3 +269,36 @@ def test_determinism_repeat(fg, handle):
     r = [handle.solve_batch(packed, w.pair_a, w.pair_b, w.costs, 300) for _ in range(3)]
     for x in r[1:]:
         assert np.array_equal(x[0], r[0][0]) and np.array_equal(x[1], r[0][1])
+
+
+# ------------------------------------------------------------------ sharded single pair (§8 a6)
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_sharded_virtual_matches_oracle(fg, oracle, G):
+    """The frontier split by parent over G shards (loopback exchange on one GPU) gives the oracle's
+    cost, mapping, children count and per-level records for every G (bit-identical)."""
+    flags = fg.FLAG_VIRTUAL_SHARDS
+    hs = fg.Handle(0, world_size=G, flags=flags)
+    hw = fg.Handle(0, world_size=G, flags=flags | fg.FLAG_DEBUG_WINDOW)
+    rng = synth.rng_for(53, G)
+    for k in range(6):
+        n1, n2 = int(rng.integers(3, 45)), int(rng.integers(3, 45))
+        g1 = synth.er_graph(rng, n1, 0.3, 3, 1 + k % 2)
+        g2 = synth.er_graph(rng, n2, 0.3, 3, 1 + k % 2)
+        K = int(rng.integers(1, 600))
+        o = oracle.kbest(g1, g2, COSTS["setting1"], K, levels=True)
+        for h in (hs, hw):
+            r = h.solve_pair(g1, g2, COSTS["setting1"], K, levels=True)
+            assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]), (G, k)
+            assert r["children"] == o["children"] and r["levels"] == [tuple(x) for x in o["levels"]]
+    hs.close()
+    hw.close()
+
+
+def test_sharded_virtual_large_pair(fg, handle):
+    """A config-4-style pair (n2 > 254, uint16 lambda): 4 virtual shards == the single-GPU path."""
+    g1, g2 = synth.large_pair(300, 0.05, seed=11)
+    ref = handle.solve_pair(g1, g2, COSTS["setting1"], 2000, levels=True)
+    h = fg.Handle(0, world_size=4, flags=fg.FLAG_VIRTUAL_SHARDS)
+    r = h.solve_pair(g1, g2, COSTS["setting1"], 2000, levels=True)
+    h.close()
+    assert r["cost"] == ref["cost"] and np.array_equal(r["mapping"], ref["mapping"]) and r["levels"] == ref["levels"]
