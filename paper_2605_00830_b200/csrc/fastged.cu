@@ -437,6 +437,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         spans.push_back({kv.first, {order_all.size(), v.size()}});
         order_all.insert(order_all.end(), v.begin(), v.end());
     }
+    CK(cudaEventRecord(h->ev_begin, h->stream));
     CK(h->stage.reserve(4 * order_all.size() + 64));
     if (!order_all.empty()) {
         memcpy(h->stage.p, order_all.data(), 4 * order_all.size());
@@ -444,7 +445,6 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         h->stats.h2d_bytes += (int64_t)(4 * order_all.size());
     }
     CK(cudaMemsetAsync(b->dwork.p, 0, 64 * sizeof(int), h->stream));
-    CK(cudaEventRecord(h->ev_begin, h->stream));
     int gi = 0;
     for (auto &sp : spans) {
         const GroupKey key = sp.first;

@@ -1,0 +1,45 @@
+"""Summarise gpurun_out/ evidence into profiles/ (launch list, ncu full metrics, hotspots, bench lines)."""
+import collections, csv, json, math, os, shutil, subprocess, sys
+R = sys.argv[1] if len(sys.argv) > 1 else "r1"
+os.makedirs("profiles", exist_ok=True)
+rows = [r for r in csv.reader(open("gpurun_out/launches.csv")) if len(r) > 10]
+hdr = rows[0]; ik = hdr.index("Kernel Name"); iv = hdr.index("Metric Value")
+agg = collections.defaultdict(list)
+for r in rows[1:]:
+    agg[r[ik]].append(float(r[iv].replace(",", "")))
+tot = sum(sum(v) for v in agg.values())
+lines = ["# ncu launch list of `python bench.py --steps 2 --warmup 1 --no-cpu-baseline` (gpu__time_duration.sum, --clock-control none)",
+         "# cold-cache, serialised replay: compare SHARES, not absolutes", "share   launches  mean_us  kernel"]
+for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+    lines.append(f"{sum(v)/tot*100:6.2f}%  {len(v):3d}  {sum(v)/len(v)/1e3:10.1f}  {k}")
+open(f"profiles/{R}_launches_bench.txt", "w").write("\n".join(lines) + "\n")
+out = subprocess.run(["ncu", "-i", "gpurun_out/prof_bench.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(out.splitlines())); hdr = r[0]; units = r[1]
+want = ['Kernel Name', 'gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'smsp__inst_executed.sum',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'launch__registers_per_thread', 'launch__shared_mem_per_block_dynamic', 'launch__grid_size']
+idx = {h: i for i, h in enumerate(hdr)}
+recs = [{w: row[idx[w]] for w in want if w in idx} for row in r[2:]]
+for x in recs:
+    x["units"] = {w: units[idx[w]] for w in want if w in idx}
+json.dump(recs, open(f"profiles/{R}_ncu_full_batch.json", "w"), indent=1)
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+dram = []
+for x in recs:
+    try:
+        v = (float(x['dram__bytes_read.sum']) + float(x['dram__bytes_write.sum'])) * scale.get(x["units"]['dram__bytes_read.sum'], 1)
+        dram.append(None if math.isnan(v) else v)
+    except Exception:
+        dram.append(None)
+valid = [d for d in dram if d is not None]
+summary = {"source": "ncu --set full --clock-control none -k regex:kbest_batch -c 3 python scripts/prof_batch.py 10000 1000 1 (the bench workload)",
+           "kernels": [x['Kernel Name'] for x in recs], "dram_bytes_per_launch": dram,
+           "bench_kernel_dram_bytes_per_launch": (sum(valid) / len(valid)) if valid else None}
+json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
+subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep '(int)2' 30 > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
+for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "time_large.txt", "nvsmi.txt"):
+    if os.path.exists(f"gpurun_out/{f}"):
+        shutil.copy(f"gpurun_out/{f}", f"profiles/{R}_{f}")
+print(open(f"profiles/{R}_launches_bench.txt").read()); print(json.dumps(summary, indent=1))
