@@ -329,10 +329,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         int r = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
-                            uint32_t F = Vm[w] & ~U[w];
-                            while (F) {
-                                const int bt = __ffs(F) - 1;
-                                F &= F - 1;
+                            auto child_code = [&](int bt) -> int {
                                 const int u = 32 * w + bt;
                                 int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
@@ -351,9 +348,23 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                                     }
                                 }
                                 const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb + c.esub * mis;
-                                const int code = rank_code(ped, base, win);
-                                crow[r++] = (uint8_t)code;
-                                hist_add(code);
+                                return rank_code(ped, base, win);
+                            };
+                            uint32_t F = Vm[w] & ~U[w];
+                            while (F) { // two free targets per iteration (independent chains)
+                                const int b0 = __ffs(F) - 1;
+                                F &= F - 1;
+                                const bool two = F != 0u;
+                                const int b1 = two ? __ffs(F) - 1 : b0;
+                                F &= F - 1;
+                                const int c0 = child_code(b0), c1 = child_code(b1);
+                                crow[r] = (uint8_t)c0;
+                                atomicAdd(&whist[c0], 1); // codes 0 and win+1 land in unused bins
+                                if (two) {
+                                    crow[r + 1] = (uint8_t)c1;
+                                    atomicAdd(&whist[c1], 1);
+                                }
+                                r += two ? 2 : 1;
                             }
                         }
                         const int cdel = rank_code(pedp + dDel, base, win); // deletion child (C5)
