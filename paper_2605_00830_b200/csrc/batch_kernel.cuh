@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
 #pragma unroll
                         for (int k = 0; k < DMAX; ++k) tl[k] = (LAB && k < d) ? (int)sT[k * Kc + p] : MAP_DEL;
                         uint8_t *crow = codes + sOff[p];
+                        const int pb = pedp - base + 1 + edd;
                         int r = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
@@ -347,8 +348,9 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                                         mis += (e != 0) & (e != s_pl[k]);
                                     }
                                 }
-                                const int ped = pedp + (((Mm[w] >> bt) & 1u) ? c.vsub : 0) + edd + c.eins * cnt - ee * cb + c.esub * mis;
-                                return rank_code(ped, base, win);
+                                // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
+                                const int x = pb + (int)((Mm[w] >> bt) & 1u) * c.vsub + c.eins * cnt - ee * cb + c.esub * mis;
+                                return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
                             while (F) { // two free targets per iteration (independent chains)
