@@ -25,8 +25,9 @@
 //      min(K, c_i) children are kept, the smallest under (PED, parent, child) (reading C12).  No sort.
 //      If the K-th smallest lies beyond the window the window slides and A is repeated.
 //   S  Selection: every thread owns a contiguous run of code words; SWAR byte compares count codes
-//      < t / == t, a block scan gives each thread its output offset and tie admissions, survivors'
-//      code indices are written in (parent, child) order (C13), then decoded to (p, j) balanced.
+//      < t / == t, a block scan gives each thread its output offset and tie admissions, survivors
+//      are written as (parent, rank within parent) in (parent, child) order (C13), then decoded to
+//      (p, j) and their PED (from the rank code) in a balanced pass.
 //   U  Update: next frontier columns with coalesced stores; while copying the
 //      lambda columns, B_p of the next level is accumulated (no separate gathers).
 // After the last level each survivor gets the insertion completion (C6) and the
@@ -36,6 +37,10 @@
 #include <cstdio>
 
 namespace fg {
+
+#ifndef FG_MINBLOCKS
+#define FG_MINBLOCKS 2 // resident CTAs per SM requested from ptxas (A/B experiments)
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAP_DEL = 255;      // lambda entry of a deleted g1 vertex
@@ -157,7 +162,7 @@ __device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, 
 }
 
 template <int W, bool LAB, int NT, bool SMEM>
-__global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
+__global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const BatchArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     __shared__ int s_hist[(NT / 32) * 129];
     __shared__ int s_tmp[144 + 32];
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
     uint8_t *s_e2 = dsmem + a.sm.e2;
     uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
     int32_t *selped = reinterpret_cast<int32_t *>(wk + a.sm.ped); // PED of survivor k (-1: recompute)
-    uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [K][W]
+    uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [W][K]
     int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
     uint8_t *sT = wk + a.sm.t;
     uint8_t *codes = wk + a.sm.codes;
@@ -206,16 +211,6 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
         const int32_t *pl = reinterpret_cast<const int32_t *>(a.blob + pd.pl);
         const uint32_t *adj2 = reinterpret_cast<const uint32_t *>(a.blob + pd.adj2);
 
-        // lane-owned adjacency rows and labels of u = lane + 32 s
-        uint32_t A[W][W];
-        int vl2r[W];
-#pragma unroll
-        for (int s = 0; s < W; ++s) {
-            const int u = lane + 32 * s;
-#pragma unroll
-            for (int w = 0; w < W; ++w) A[s][w] = (u < n2) ? __ldg(adj2 + u * W + w) : 0u;
-            vl2r[s] = (u < n2) ? __ldg(vl2 + u) : 0;
-        }
         for (int x = threadIdx.x; x < n2 * W; x += NT) sAdj[x] = __ldg(adj2 + x);
         if (LAB) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
@@ -257,13 +252,13 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             }
             for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
             const int vl1i = __ldg(vl1 + i);
-            int cv[W];
             uint32_t Vm[W], Mm[W]; // existing targets / label mismatches, bit u of word u >> 5
 #pragma unroll
             for (int s = 0; s < W; ++s) {
-                cv[s] = (vl2r[s] == vl1i) ? 0 : c.vsub;
-                Vm[s] = __ballot_sync(FULL, lane + 32 * s < n2);
-                Mm[s] = __ballot_sync(FULL, lane + 32 * s < n2 && vl2r[s] != vl1i);
+                const int u = lane + 32 * s;
+                const int l2 = (u < n2) ? __ldg(vl2 + u) : 0;
+                Vm[s] = __ballot_sync(FULL, u < n2);
+                Mm[s] = __ballot_sync(FULL, u < n2 && l2 != vl1i);
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
             block_sync(); // P_i list and zeroed histograms visible
@@ -271,18 +266,21 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             // ---------------- P: parents -> used masks in shared memory, compact code offsets ----------------
             // Parent p has f_p = n2 - |used_p| substitution children + 1 deletion child; its rank codes
             // occupy codes[off_p, off_p + f_p + 1) in (target ascending, deletion last) = lin order.
-            const int ppt = (N + NT - 1) / NT;
+            // odd run length: lane t touches parent t*ppt + x, conflict-free across the banks
+            const int ppt = ((N + NT - 1) / NT) | 1;
             const int pb = min(N, threadIdx.x * ppt), pe = min(N, pb + ppt);
+            // parent p's codes occupy [off_p, off_p + f_p + 1): its free targets ascending, then the deletion
+            auto row_bytes = [&](int p) {
+                int nc = 1;
+#pragma unroll
+                for (int w = 0; w < W; ++w) nc += __popc(Vm[w] & ~sU[w * Kc + p]);
+                return nc;
+            };
             int nloc = 0;
             for (int p = pb; p < pe; ++p) {
-                int usedc = 0;
 #pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    const uint32_t U = PusedT[(int64_t)w * Kc + p];
-                    sU[p * W + w] = U;
-                    usedc += __popc(U);
-                }
-                nloc += n2 - usedc + 1;
+                for (int w = 0; w < W; ++w) sU[w * Kc + p] = PusedT[(int64_t)w * Kc + p];
+                nloc += row_bytes(p);
                 if (LAB) {
                     const int dd = min(d, DMAX);
                     for (int k = 0; k < dd; ++k) sT[k * Kc + p] = PmapT[(int64_t)s_pq[k] * Kc + p];
@@ -292,10 +290,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             block_scan2<NT>(nloc, 0, obase, dummy, ci, dummy2, s_tmp); // ci = candidates of the level
             for (int p = pb; p < pe; ++p) {
                 sOff[p] = obase;
-                int usedc = 0;
-#pragma unroll
-                for (int w = 0; w < W; ++w) usedc += __popc(sU[p * W + w]);
-                obase += n2 - usedc + 1;
+                obase += row_bytes(p);
             }
             if (threadIdx.x == 0) {
                 sOff[N] = ci;
@@ -321,7 +316,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         uint32_t U[W], B[W];
                         // B_p: images of the earlier g1 neighbours of v_i (replaces VFrom/VTo)
 #pragma unroll
-                        for (int w = 0; w < W; ++w) { U[w] = sU[p * W + w]; B[w] = LAB ? 0u : PBT[(int64_t)w * Kc + p]; }
+                        for (int w = 0; w < W; ++w) { U[w] = sU[w * Kc + p]; B[w] = LAB ? 0u : PBT[(int64_t)w * Kc + p]; }
                         int tl[DMAX]; // labelled edges: the images t_k themselves (d <= DMAX)
 #pragma unroll
                         for (int k = 0; k < DMAX; ++k) tl[k] = (LAB && k < d) ? (int)sT[k * Kc + p] : MAP_DEL;
@@ -379,7 +374,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                         const int pedp = Pped[p];
                         uint32_t U[W];
 #pragma unroll
-                        for (int w = 0; w < W; ++w) U[w] = sU[p * W + w];
+                        for (int w = 0; w < W; ++w) U[w] = sU[w * Kc + p];
                         int ped_s[W];
                         if (!LAB) {
                             uint32_t B[W];
@@ -390,10 +385,11 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                                 int cnt = 0, cb = 0;
 #pragma unroll
                                 for (int w = 0; w < W; ++w) {
-                                    cnt += __popc(A[s][w] & U[w]);
-                                    cb += __popc(A[s][w] & B[w]);
+                                    const uint32_t rw = (lane + 32 * s < n2) ? sAdj[(lane + 32 * s) * W + w] : 0u;
+                                    cnt += __popc(rw & U[w]);
+                                    cb += __popc(rw & B[w]);
                                 }
-                                ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb;
+                                ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - ee * cb;
                             }
                         } else {
                             int cb[W], mis[W];
@@ -416,8 +412,9 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                             for (int s = 0; s < W; ++s) {
                                 int cnt = 0;
 #pragma unroll
-                                for (int w = 0; w < W; ++w) cnt += __popc(A[s][w] & U[w]);
-                                ped_s[s] = pedp + cv[s] + edd + c.eins * cnt - ee * cb[s] + c.esub * mis[s];
+                                for (int w = 0; w < W; ++w)
+                                    cnt += __popc(((lane + 32 * s < n2) ? sAdj[(lane + 32 * s) * W + w] : 0u) & U[w]);
+                                ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - ee * cb[s] + c.esub * mis[s];
                             }
                         }
                         uint8_t *crow = codes + sOff[p];
@@ -488,7 +485,8 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             {
                 const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes);
                 const int nwords = (ci + 3) >> 2;
-                const int seg = (nwords + NT - 1) / NT;
+                // odd segment length: lane t reads word t*seg + x, conflict-free across the 32 banks
+                const int seg = ((nwords + NT - 1) / NT) | 1;
                 const int w0 = min(nwords, threadIdx.x * seg), w1 = min(nwords, w0 + seg);
                 if (keepall) { tcode = 256; rq = 0; }
                 // SWAR byte masks (codes are 0..win+1 <= 128 or 255): bit 7 of each byte set where
@@ -510,27 +508,35 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                 block_scan2<NT>(lt, eq, ltpre, eqpre, lttot, eqtot, s_tmp);
                 Nn = keepall ? lttot : K;
                 int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
-                if (lt + eq > 0) {
+                if (lt + (eqpre < rq ? eq : 0) > 0) {
+                    // parent cursor: the last p with off_p <= 4 w0 (then advanced monotonically)
+                    int pc = 0, phi = N - 1;
+                    while (pc < phi) {
+                        const int mid = (pc + phi + 1) >> 1;
+                        if (sOff[mid] <= 4 * w0) pc = mid; else phi = mid - 1;
+                    }
+                    int off0 = sOff[pc], off1 = sOff[pc + 1];
                     for (int x = w0; x < w1; ++x) {
                         const uint32_t v = cw[x];
-                        uint32_t mlt, meq = 0u;
-                        if (keepall) mlt = valid(v);
+                        uint32_t m;
+                        if (keepall) m = valid(v);
                         else {
                             const uint32_t g0 = ge(v, t4);
-                            mlt = ~g0 & 0x80808080u;
-                            meq = g0 & ~ge(v, t41);
+                            m = ~g0 & 0x80808080u;
+                            uint32_t meq = g0 & ~ge(v, t41);
+                            if (meq) { // ties at t are admitted in code order up to the quota rq
+                                const int ne = __popc(meq);
+                                if (eq_seen + ne <= rq) m |= meq;
+                                else
+                                    for (int z = rq - eq_seen; z > 0; --z) { const uint32_t low = meq & (0u - meq); m |= low; meq ^= low; }
+                                eq_seen += ne;
+                            }
                         }
-                        uint32_t m = mlt | meq;
                         while (m) {
-                            const int bit = __ffs(m) - 1;
+                            const int idx = 4 * x + ((__ffs(m) - 1) >> 3);
                             m &= m - 1;
-                            bool keep = (mlt >> bit) & 1u;
-                            if (!keep) { keep = eq_seen < rq; eq_seen++; }
-                            if (!keep) continue;
-                            const int code = (int)((v >> (bit & ~7)) & 0xffu);
-                            sel[out] = (uint32_t)(4 * x + (bit >> 3)); // compact code index; decoded below
-                            selped[out] = (code >= 1 && code <= win) ? base + code - 1 : -1;
-                            ++out;
+                            while (off1 <= idx) { off0 = off1; off1 = sOff[++pc + 1]; }
+                            sel[out++] = ((uint32_t)pc << 8) | (uint32_t)(idx - off0); // (parent, rank in parent)
                         }
                     }
                 }
@@ -545,27 +551,23 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
             }
             block_sync();
 
-            // ---------------- decode survivors: compact code index -> (parent p, child j) ----------------
+            // ---------------- decode survivors: (parent p, rank in p) -> (p, child j), PED from the code ----------------
             for (int k = threadIdx.x; k < Nn; k += NT) {
-                const int cidx = (int)sel[k];
-                int plo = 0, phi = N - 1; // last p with off_p <= cidx
-                while (plo < phi) {
-                    const int mid = (plo + phi + 1) >> 1;
-                    if (sOff[mid] <= cidx) plo = mid; else phi = mid - 1;
-                }
-                const int rnk = cidx - sOff[plo], f = sOff[plo + 1] - sOff[plo] - 1;
-                int j = n2;
-                if (rnk < f) { // the rnk-th free target of parent plo
-                    int rr = rnk;
+                const uint32_t v = sel[k];
+                const int p = (int)(v >> 8), rnk = (int)(v & 255u);
+                const int off = sOff[p];
+                const int code = codes[off + rnk];
+                selped[k] = (code >= 1 && code <= win) ? base + code - 1 : -1;
+                int j = n2; // past every target: the deletion child
+                int rr = rnk;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        const uint32_t F = Vm[w] & ~sU[plo * W + w];
-                        const int cnt = __popc(F);
-                        if (rr >= 0 && rr < cnt) j = 32 * w + select_bit(F, rr);
-                        rr -= cnt;
-                    }
+                for (int w = 0; w < W; ++w) {
+                    const uint32_t F = Vm[w] & ~sU[w * Kc + p];
+                    const int cnt = __popc(F);
+                    if (rr >= 0 && rr < cnt) j = 32 * w + select_bit(F, rr);
+                    rr -= cnt;
                 }
-                sel[k] = ((uint32_t)plo << 8) | (uint32_t)j;
+                sel[k] = ((uint32_t)p << 8) | (uint32_t)j;
             }
             block_sync();
 
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                     else {
                         int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
-                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & sU[p * W + w]);
+                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & sU[w * Kc + p]);
                         if (!LAB) {
 #pragma unroll
                             for (int w = 0; w < W; ++w) cb += __popc(sAdj[j * W + w] & PBT[(int64_t)w * Kc + p]);
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(NT) kbest_batch_kernel(const BatchArgs a) {
                 const int w = x / Nn, k = x - w * Nn;
                 const uint32_t v = sel[k];
                 const int p = (int)(v >> 8), j = (int)(v & 255u);
-                QusedT[(int64_t)w * Kc + k] = sU[p * W + w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+                QusedT[(int64_t)w * Kc + k] = sU[w * Kc + p] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
             }
             {
                 const int nk4 = (Nn + 3) >> 2;

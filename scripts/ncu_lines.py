@@ -22,3 +22,17 @@ tot_i = sum(v[0] for v in agg.values()) or 1; tot_s = sum(v[1] for v in agg.valu
 print(f"total warp-instructions {tot_i:.3e}, stall samples {tot_s}")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
     print(f"{100*v[1]/tot_s:5.1f}% samp {100*v[0]/tot_i:5.1f}% inst  L{k[1]:4d}  {v[2]}")
+
+# phase totals: source lines grouped by the "// ---------------- <phase>" markers of the kernel file
+if len(sys.argv) > 4:
+    src = open(sys.argv[4]).read().splitlines()
+    marks = [(n + 1, l.strip().strip("/- ").split(":")[0][:40]) for n, l in enumerate(src) if "// ----------------" in l]
+    ph = collections.defaultdict(lambda: [0, 0])
+    for k, v in agg.items():
+        name = "pre"
+        for ln, nm in marks:
+            if k[1] >= ln: name = nm
+        if k[1] < 160 or k[1] > len(src): name = "helpers(<160)"
+        ph[name][0] += v[0]; ph[name][1] += v[1]
+    for nm, v in sorted(ph.items(), key=lambda kv: -kv[1][1]):
+        print(f"PHASE {nm:42s} samp {100*v[1]/tot_s:5.1f}%  inst {100*v[0]/tot_i:5.1f}%")
