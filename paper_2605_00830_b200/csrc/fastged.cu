@@ -114,6 +114,9 @@ struct fastged_batch {
     int64_t total_map = 0;
     int n1max = 0, n2max = 0;
     DevBuf blob, ddesc, dorder, dcost, dmap, dchild, dpar, dalg, dwork;
+    HostPinned stage; // this batch's pinned staging (inputs, order, results): batches can be in flight together
+    size_t ord_at = 0, res_at = 0; // byte offsets of the order and result areas in `stage`
+    int32_t pair_base = 0;         // index of pair 0 in the caller's arrays (error messages)
     std::map<GroupKey, std::vector<int32_t>> groups; // pair indices per kernel variant
     std::vector<int32_t> large;                      // pairs beyond the batched limits
     bool ran = false;
@@ -135,7 +138,7 @@ struct fastged_handle {
     int evused = 0;
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     DevBuf lblob, lbuf; // large single-pair mode
-    fastged_batch *tmp = nullptr; // reused by solve_batch / solve_pair
+    fastged_batch *tmp = nullptr, *tmp2 = nullptr; // reused by solve_batch (two pipelined chunks) / solve_pair
     ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1, NCCL transport)
 };
 
@@ -292,15 +295,24 @@ cudaEvent_t next_event(fastged_handle_t *h) {
 }
 
 // ---------------------------------------------------------------- batch build
+void free_batch(fastged_batch *b) {
+    if (!b) return;
+    b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
+    b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
+    b->stage.release();
+    delete b;
+}
+
 // Validates, packs and uploads a batch.  `reuse` (optional) is a batch whose device buffers are
 // recycled (solve_batch keeps one per handle, so repeated calls do no cudaMalloc/cudaFree).
 fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph_t *g1s,
-                           const fastged_graph_t *g2s, fastged_batch *reuse = nullptr) {
+                           const fastged_graph_t *g2s, fastged_batch *reuse = nullptr, int32_t pair_base = 0) {
     if (npairs < 0) fail(FASTGED_ERR_ARG, "npairs < 0");
     if (npairs > 0 && (!g1s || !g2s)) fail(FASTGED_ERR_ARG, "graph arrays are NULL");
     fastged_batch *b = reuse ? reuse : new fastged_batch();
     b->ran = false;
     b->n1max = b->n2max = 0;
+    b->pair_base = pair_base;
     try {
         b->npairs = npairs;
         b->descs.resize(npairs);
@@ -318,8 +330,8 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
 #pragma omp parallel for schedule(dynamic, 64)
         for (int p = 0; p < npairs; ++p) {
             try {
-                validate_graph(&g1s[p], p, "g1");
-                validate_graph(&g2s[p], p, "g2");
+                validate_graph(&g1s[p], pair_base + p, "g1");
+                validate_graph(&g2s[p], pair_base + p, "g2");
                 lab[p] = labelled_pair(&g1s[p], &g2s[p]);
                 n2p[p] = (g2s[p].n + 3) & ~3;
                 sz[p] = (int64_t)pair_blob_bytes(&g1s[p], &g2s[p], lab[p], n2p[p]);
@@ -338,12 +350,14 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         b->total_map = b->map_off[npairs];
         size_t blob_bytes = (size_t)off[npairs];
         size_t desc_bytes = sizeof(fg::PairDesc) * (size_t)std::max(npairs, 1);
-        CK(h->stage.reserve(blob_bytes + desc_bytes + 64));
-        uint8_t *stage = (uint8_t *)h->stage.p;
+        b->ord_at = align16(blob_bytes + desc_bytes);
+        b->res_at = align16(b->ord_at + 4 * (size_t)npairs);
+        CK(b->stage.reserve(b->res_at + 32 * (size_t)npairs + 4 * (size_t)b->total_map + 64));
+        uint8_t *stage = (uint8_t *)b->stage.p;
 #pragma omp parallel for schedule(dynamic, 64)
         for (int p = 0; p < npairs; ++p) {
             try {
-                pack_pair(&g1s[p], &g2s[p], lab[p], n2p[p], stage, off[p], b->descs[p], p);
+                pack_pair(&g1s[p], &g2s[p], lab[p], n2p[p], stage, off[p], b->descs[p], pair_base + p);
             } catch (const FgError &e) {
 #pragma omp critical(fg_err)
                 if (p < bad) { bad = p; perr[0] = e; }
@@ -366,13 +380,11 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         if (npairs) CK(cudaMemcpyAsync(b->ddesc.p, stage + blob_bytes, sizeof(fg::PairDesc) * npairs,
                                        cudaMemcpyHostToDevice, h->stream));
         h->stats.h2d_bytes += (int64_t)(blob_bytes + sizeof(fg::PairDesc) * npairs);
-        CK(cudaStreamSynchronize(h->stream)); // staging buffer is reused by the next call
-        return b;
+        return b; // b->stage stays in use until the stream passes the copies (the next sync on it)
     } catch (...) {
         if (!reuse) {
-            b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
-            b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
-            delete b;
+            cudaStreamSynchronize(h->stream);
+            free_batch(b);
         }
         throw;
     }
@@ -389,6 +401,7 @@ int64_t frontier_cap(int n1, int n2, int64_t k) {
 }
 
 constexpr int BATCH_NT = 256;
+constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batches into two pipelined chunks
 
 void *batch_kernel_for(int W, bool lab, bool smem) {
 #define KV(WW, LL, SS) \
@@ -401,8 +414,10 @@ void *batch_kernel_for(int W, bool lab, bool smem) {
     return nullptr;
 }
 
+// first = false appends to the timing/launch stats of a preceding run_batch on the same stream
+// (pipelined chunks of one solve_batch call).
 void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, int64_t k,
-               int64_t *levels_dev) {
+               int64_t *levels_dev, bool first = true) {
     validate_costs(c);
     if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
     // group pairs by kernel variant; schedule the largest pairs first (dynamic counter)
@@ -413,7 +428,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         int64_t bound = (int64_t)d.n1 * std::max(c->vsub, c->vdel) + (int64_t)d.n2 * c->vins +
                         ((int64_t)d.m1 + d.m2) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
         if (bound >= ((int64_t)1 << 31))
-            fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", p, (long long)bound);
+            fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
         if (d.n2 <= 128 && d.n1 <= 1024 && k <= (1 << 24))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
@@ -421,11 +436,13 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
     }
     if (!b->large.empty())
         fail(FASTGED_ERR_CAPACITY, "pair %d exceeds the batched limits (n2 <= 128, n1 <= 1024, k <= 2^24); "
-                                   "solve it with fastged_solve_pair", b->large[0]);
-    h->evused = 0;
-    h->stats.kernel_launches = 0;
-    h->stats.branch_launches = 0;
-    h->stats.branch_ms = 0.f;
+                                   "solve it with fastged_solve_pair", b->pair_base + b->large[0]);
+    if (first) {
+        h->evused = 0;
+        h->stats.kernel_launches = 0;
+        h->stats.branch_launches = 0;
+        h->stats.branch_ms = 0.f;
+    }
     std::vector<int32_t> order_all;
     std::vector<std::pair<GroupKey, std::pair<size_t, size_t>>> spans;
     for (auto &kv : b->groups) {
@@ -437,11 +454,12 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         spans.push_back({kv.first, {order_all.size(), v.size()}});
         order_all.insert(order_all.end(), v.begin(), v.end());
     }
-    CK(cudaEventRecord(h->ev_begin, h->stream));
-    CK(h->stage.reserve(4 * order_all.size() + 64));
+    if (first) CK(cudaEventRecord(h->ev_begin, h->stream));
+    // the order goes behind the blob in this batch's staging (the blob's bytes may still be in flight)
+    uint8_t *ord = (uint8_t *)b->stage.p + b->ord_at;
     if (!order_all.empty()) {
-        memcpy(h->stage.p, order_all.data(), 4 * order_all.size());
-        CK(cudaMemcpyAsync(b->dorder.p, h->stage.p, 4 * order_all.size(), cudaMemcpyHostToDevice, h->stream));
+        memcpy(ord, order_all.data(), 4 * order_all.size());
+        CK(cudaMemcpyAsync(b->dorder.p, ord, 4 * order_all.size(), cudaMemcpyHostToDevice, h->stream));
         h->stats.h2d_bytes += (int64_t)(4 * order_all.size());
     }
     CK(cudaMemsetAsync(b->dwork.p, 0, 64 * sizeof(int), h->stream));
@@ -555,14 +573,11 @@ void finish_timing(fastged_handle_t *h) {
     }
 }
 
-void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t *mappings_out,
-              int64_t *children_out) {
+// Enqueue the D2H copies of a batch's results into its staging (no sync).
+void download_enqueue(fastged_handle_t *h, fastged_batch *b) {
     if (!b->ran) fail(FASTGED_ERR_ARG, "batch was not run");
-    if (b->npairs > 0 && !costs_out) fail(FASTGED_ERR_ARG, "costs_out is NULL");
-    if (b->total_map > 0 && !mappings_out) fail(FASTGED_ERR_ARG, "mappings_out is NULL");
     const size_t P = (size_t)b->npairs, M = (size_t)b->total_map;
-    CK(h->stage.reserve(8 * P * 4 + 4 * M + 64));
-    uint8_t *st = (uint8_t *)h->stage.p;
+    uint8_t *st = (uint8_t *)b->stage.p + b->res_at;
     int64_t *hc = (int64_t *)st, *hch = hc + P, *hpa = hch + P, *hal = hpa + P;
     int32_t *hm = (int32_t *)(hal + P);
     if (P) {
@@ -572,9 +587,16 @@ void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t
         CK(cudaMemcpyAsync(hal, b->dalg.p, 8 * P, cudaMemcpyDeviceToHost, h->stream));
     }
     if (M) CK(cudaMemcpyAsync(hm, b->dmap.p, 4 * M, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    finish_timing(h);
     h->stats.d2h_bytes += (int64_t)(32 * P + 4 * M);
+}
+
+// After the stream sync: copy a batch's results out and add its counters to the stats.
+void download_collect(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t *mappings_out,
+                      int64_t *children_out) {
+    const size_t P = (size_t)b->npairs, M = (size_t)b->total_map;
+    uint8_t *st = (uint8_t *)b->stage.p + b->res_at;
+    int64_t *hc = (int64_t *)st, *hch = hc + P, *hpa = hch + P, *hal = hpa + P;
+    int32_t *hm = (int32_t *)(hal + P);
     if (P) memcpy(costs_out, hc, 8 * P);
     if (M) memcpy(mappings_out, hm, 4 * M);
     if (children_out && P) memcpy(children_out, hch, 8 * P);
@@ -583,17 +605,25 @@ void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t
         ch += hch[p]; pa += hpa[p]; al += hal[p];
         ops += hch[p] * (4 * (int64_t)b->W[p] + 8); // popcount-form lane-ops per child
     }
-    h->stats.children_evaluated = ch;
-    h->stats.parents_expanded = pa;
-    h->stats.alg_bytes = al;
-    h->stats.alg_ops = ops;
+    h->stats.children_evaluated += ch;
+    h->stats.parents_expanded += pa;
+    h->stats.alg_bytes += al;
+    h->stats.alg_ops += ops;
 }
 
-void free_batch(fastged_batch *b) {
-    if (!b) return;
-    b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
-    b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
-    delete b;
+void check_outputs(const fastged_batch *b, int64_t *costs_out, int32_t *mappings_out) {
+    if (b->npairs > 0 && !costs_out) fail(FASTGED_ERR_ARG, "costs_out is NULL");
+    if (b->total_map > 0 && !mappings_out) fail(FASTGED_ERR_ARG, "mappings_out is NULL");
+}
+
+void download(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out, int32_t *mappings_out,
+              int64_t *children_out) {
+    check_outputs(b, costs_out, mappings_out);
+    download_enqueue(h, b);
+    CK(cudaStreamSynchronize(h->stream));
+    finish_timing(h);
+    h->stats.children_evaluated = h->stats.parents_expanded = h->stats.alg_bytes = h->stats.alg_ops = 0;
+    download_collect(h, b, costs_out, mappings_out, children_out);
 }
 
 void begin_call(fastged_handle_t *h) {
@@ -790,6 +820,7 @@ void fastged_destroy(fastged_handle_t *h) {
     h->lblob.release();
     h->lbuf.release();
     free_batch(h->tmp);
+    free_batch(h->tmp2);
     h->scratch.release();
     h->levels.release();
     h->stage.release();
@@ -870,9 +901,27 @@ int fastged_solve_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph
         validate_costs(c);
         if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
         if (!h->tmp) h->tmp = new fastged_batch();
-        fastged_batch *b = build_batch(h, npairs, g1s, g2s, h->tmp);
-        run_batch(h, b, c, k, nullptr);
-        download(h, b, costs_out, mappings_out, children_out);
+        // Two pipelined chunks: the GPU starts on a small first chunk while the host validates and
+        // packs the rest (same stream, so the second chunk's copies and kernels queue behind it).
+        // Pairs are independent, so the chunking does not change any result.
+        const int32_t n0 = npairs >= PIPELINE_MIN_PAIRS ? std::max<int32_t>(npairs / 8, 512) : npairs;
+        fastged_batch *b0 = build_batch(h, n0, g1s, g2s, h->tmp);
+        run_batch(h, b0, c, k, nullptr, true);
+        fastged_batch *b1 = nullptr;
+        if (n0 < npairs) {
+            if (!h->tmp2) h->tmp2 = new fastged_batch();
+            b1 = build_batch(h, npairs - n0, g1s + n0, g2s + n0, h->tmp2, n0);
+            run_batch(h, b1, c, k, nullptr, false);
+        }
+        check_outputs(b0, costs_out, mappings_out);
+        download_enqueue(h, b0);
+        if (b1) download_enqueue(h, b1);
+        CK(cudaStreamSynchronize(h->stream));
+        finish_timing(h);
+        download_collect(h, b0, costs_out, mappings_out, children_out);
+        if (b1)
+            download_collect(h, b1, costs_out + n0, mappings_out ? mappings_out + b0->total_map : nullptr,
+                             children_out ? children_out + n0 : nullptr);
         return FASTGED_OK;
     } catch (const FgError &e) {
         cudaStreamSynchronize(h->stream);

@@ -263,6 +263,27 @@ def test_device_resident_split_matches_solve_batch(fg, handle):
         assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) and np.array_equal(x[3], y[3])
 
 
+def test_pipelined_solve_batch(fg, handle):
+    """solve_batch splits >= 4096 pairs into two pipelined chunks: same results as one resident batch,
+    and a bad pair in the second chunk is reported with its global index."""
+    w = synth.config_workload(2, npairs=5000)
+    packed = fg.PackedGraphs(w.graphs)
+    a = handle.solve_batch(packed, w.pair_a, w.pair_b, w.costs, w.K)
+    st = handle.stats()
+    assert st["children_evaluated"] == int(np.sum(a[3])) and st["kernel_launches"] >= 2
+    b = handle.upload(packed, w.pair_a, w.pair_b)
+    b.run(w.costs, w.K)
+    r = b.download()
+    b.free()
+    assert np.array_equal(a[0], r[0]) and np.array_equal(a[1], r[1]) and np.array_equal(a[2], r[2])
+    assert np.array_equal(a[3], r[3])
+    g = synth.path_graph(4)
+    pairs = [(g, g)] * 4999 + [(g, Graph(2, [0, 0], [[1, 1]]))]
+    with pytest.raises(fg.FastGedError) as e:
+        gpu_batch(fg, handle, pairs, COSTS["unit"], 4)
+    assert "pair 4999" in str(e.value)
+
+
 def test_determinism_repeat(fg, handle):
     w = synth.config_workload(3, npairs=50, variant="unlabeled")
     packed = fg.PackedGraphs(w.graphs)
