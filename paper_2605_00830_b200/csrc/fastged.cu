@@ -642,69 +642,119 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const int Kc = (int)Kc64;
     const bool lab = labelled_pair(g1, g2);
     const int n2p = (n2 + 3) & ~3;
-    const size_t blob_bytes = pair_blob_bytes(g1, g2, lab, n2p);
+    const int W = words_for(n2);
+    const int cs = (n2 + 1 + 127) & ~127; // code / counter row stride: lane l owns u = 128 s + 4 l + b
+    // g2 extras behind the packed pair: CSR neighbour lists (label id in the high half) and the
+    // transposed bit rows adjT[W][cs] (bit u' of adjT[w][u] = edge (u, 32 w + u'))
+    const size_t base_bytes = pair_blob_bytes(g1, g2, lab, n2p);
+    const size_t o_nptr = base_bytes, o_nbr = o_nptr + align16(4 * (size_t)(n2 + 1));
+    const size_t o_adjT = o_nbr + align16(8 * (size_t)g2->m + 4);
+    const size_t blob_bytes = o_adjT + 4 * (size_t)W * cs;
     CK(h->stage.reserve(blob_bytes + 64));
+    uint8_t *st = (uint8_t *)h->stage.p;
     fg::PairDesc pd{};
-    pack_pair(g1, g2, lab, n2p, (uint8_t *)h->stage.p, 0, pd, 0);
+    pack_pair(g1, g2, lab, n2p, st, 0, pd, 0);
     pd.map_out = 0;
+    int maxdeg = 0;
+    {
+        int32_t *nptr = (int32_t *)(st + o_nptr);
+        uint32_t *nbr = (uint32_t *)(st + o_nbr);
+        uint32_t *adjT = (uint32_t *)(st + o_adjT);
+        const uint32_t *adj2 = (const uint32_t *)(st + pd.adj2);
+        const uint8_t *e2 = lab ? st + pd.e2lab : nullptr;
+        std::vector<int> deg(n2 + 1, 0);
+        for (int e = 0; e < g2->m; ++e) { deg[g2->edges[2 * e]]++; deg[g2->edges[2 * e + 1]]++; }
+        nptr[0] = 0;
+        for (int u = 0; u < n2; ++u) { nptr[u + 1] = nptr[u] + deg[u]; maxdeg = std::max(maxdeg, deg[u]); }
+        std::vector<int> fill(nptr, nptr + n2);
+        for (int e = 0; e < g2->m; ++e) {
+            const int x = g2->edges[2 * e], y = g2->edges[2 * e + 1];
+            const uint32_t l = lab ? (uint32_t)e2[(size_t)x * n2p + y] : 0u;
+            nbr[fill[x]++] = (uint32_t)y | (l << 16);
+            nbr[fill[y]++] = (uint32_t)x | (l << 16);
+        }
+        memset(adjT, 0, 4 * (size_t)W * cs);
+        for (int u = 0; u < n2; ++u)
+            for (int w = 0; w < W; ++w) adjT[(size_t)w * cs + u] = adj2[(size_t)u * W + w];
+    }
     CK(h->lblob.reserve(blob_bytes + 16));
     CK(cudaMemcpyAsync(h->lblob.p, h->stage.p, blob_bytes, cudaMemcpyHostToDevice, h->stream));
     h->stats.h2d_bytes += (int64_t)blob_bytes;
 
-    const int W = words_for(n2), Wp = std::max(32, (n2 + 31) & ~31);
-    const bool wide = n2 > 254;
-    const int esz = wide ? 2 : 1;
+    const bool wide = n2 > 254;          // lambda entries: uint16 (255 would collide with "deleted")
+    const bool c16 = maxdeg > 255;       // counters: uint16 when a degree does not fit a byte
+    const int esz = wide ? 2 : 1, csz = c16 ? 2 : 1;
     const int n1s = wide ? std::max(2, (n1 + 1) & ~1) : std::max(4, (n1 + 3) & ~3);
-    const int cs = (n2 + 1 + 3) & ~3;
-    size_t smem_masks = 8 * 3 * (size_t)W * 4;
-    size_t smem_adj = (size_t)W * Wp * 4;
-    int adj_in_smem = (smem_masks + smem_adj <= 160 * 1024) ? 1 : 0;
-    size_t smem = smem_masks + (adj_in_smem ? smem_adj : 0);
-    // occupancy -> cooperative grid
-    int occ = 0;
+    int dmax = 0;
+    {
+        std::vector<int> dd(n1 + 1, 0);
+        for (int e = 0; e < g1->m; ++e) dd[std::max(g1->edges[2 * e], g1->edges[2 * e + 1])]++;
+        for (int x : dd) dmax = std::max(dmax, x);
+    }
+    const int n1r = std::max(4, (dmax + 3) & ~3);
+    bool adjT_in_smem = fg::large_smem_bytes(cs, n1r, W, true) <= (size_t)h->smem_optin;
+    const size_t smem = fg::large_smem_bytes(cs, n1r, W, adjT_in_smem);
+    if (smem > (size_t)h->smem_optin) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
     void *kfn = nullptr;
-    if (wide) kfn = lab ? (void *)fg::kbest_large_kernel<uint16_t, true> : (void *)fg::kbest_large_kernel<uint16_t, false>;
-    else kfn = lab ? (void *)fg::kbest_large_kernel<uint8_t, true> : (void *)fg::kbest_large_kernel<uint8_t, false>;
+#define LK(M, C, L) (void *)fg::kbest_large_kernel<M, C, L>
+    if (wide) kfn = c16 ? (lab ? LK(uint16_t, uint16_t, true) : LK(uint16_t, uint16_t, false))
+                        : (lab ? LK(uint16_t, uint8_t, true) : LK(uint16_t, uint8_t, false));
+    else kfn = c16 ? (lab ? LK(uint8_t, uint16_t, true) : LK(uint8_t, uint16_t, false))
+                   : (lab ? LK(uint8_t, uint8_t, true) : LK(uint8_t, uint8_t, false));
+#undef LK
+    int occ = 0;
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, fg::LNT, smem));
     if (occ < 1) fail(FASTGED_ERR_CAPACITY, "large-mode kernel does not fit on an SM (smem %zu)", smem);
-    occ = std::min(occ, 4);
+    occ = std::min(occ, 2);
     const int grid = occ * h->sms;
-    const int GW = grid * 8;
+    const int GW = grid * (fg::LNT / 32);
     // device buffers
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
     size_t o_ped0 = take(4 * (size_t)Kc), o_ped1 = take(4 * (size_t)Kc);
     size_t o_used0 = take(4 * (size_t)Kc * W), o_used1 = take(4 * (size_t)Kc * W);
+    size_t o_cnt0 = take((size_t)csz * cs * Kc), o_cnt1 = take((size_t)csz * cs * Kc);
     size_t o_map0 = take((size_t)esz * n1s * Kc), o_map1 = take((size_t)esz * n1s * Kc);
     size_t o_codes = take((size_t)Kc * cs), o_selp = take(4 * (size_t)Kc), o_selj = take(4 * (size_t)Kc);
-    size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1)), o_lo = take(4 * (size_t)(n1 + 2));
-    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(24);
+    size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1));
+    size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
+    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(32);
     size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
     CK(h->lbuf.reserve(off));
     uint8_t *B = (uint8_t *)h->lbuf.p;
     CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
     CK(cudaMemsetAsync(B + o_ci, 0, 8 * (size_t)(n1 + 1), h->stream));
     CK(cudaMemsetAsync(B + o_lo, 0x7f, 4 * (size_t)(n1 + 2), h->stream));
+    CK(cudaMemsetAsync(B + o_hi, 0x80, 4 * (size_t)(n1 + 2), h->stream));
     CK(cudaMemsetAsync(B + o_best, 0xff, 8, h->stream));
+    const uint8_t *dblob = (const uint8_t *)h->lblob.p;
     fg::LargeArgs a{};
-    a.blob = (const uint8_t *)h->lblob.p;
+    a.blob = dblob;
     a.pd = pd;
     a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
     a.K = Kc;
     a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
     a.W = W;
-    a.Wp = Wp;
+    a.cs = cs;
+    a.S = cs / 128;
     a.n1s = n1s;
-    a.adj_in_smem = adj_in_smem;
+    a.n1r = n1r;
+    a.adjT_in_smem = adjT_in_smem ? 1 : 0;
+    a.degw = std::max(1, (n2 ? (2 * g2->m + n2 - 1) / n2 : 0) + 31) / 32;
+    a.nptr = (const int32_t *)(dblob + o_nptr);
+    a.nbr = (const uint32_t *)(dblob + o_nbr);
+    a.adjT = (const uint32_t *)(dblob + o_adjT);
     a.ped[0] = (int32_t *)(B + o_ped0); a.ped[1] = (int32_t *)(B + o_ped1);
     a.used[0] = (uint32_t *)(B + o_used0); a.used[1] = (uint32_t *)(B + o_used1);
+    a.cnt[0] = B + o_cnt0; a.cnt[1] = B + o_cnt1;
     a.map[0] = B + o_map0; a.map[1] = B + o_map1;
     a.codes = B + o_codes;
     a.sel_p = (int32_t *)(B + o_selp); a.sel_j = (int32_t *)(B + o_selj);
     a.hist = (int32_t *)(B + o_hist);
     a.ci = (int64_t *)(B + o_ci);
     a.lo = (int32_t *)(B + o_lo);
+    a.hi = (int32_t *)(B + o_hi);
     a.wlt = (int32_t *)(B + o_wlt); a.weq = (int32_t *)(B + o_weq);
     a.best = (unsigned long long *)(B + o_best);
     a.out = (int64_t *)(B + o_out);
@@ -715,7 +765,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     CK(cudaEventRecord(h->ev_begin, h->stream));
     CK(cudaEventRecord(e0, h->stream));
     void *params[] = {(void *)&a};
-    CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(256), params, smem, h->stream));
+    CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(fg::LNT), params, smem, h->stream));
     CK(cudaEventRecord(e1, h->stream));
     CK(cudaEventRecord(h->ev_end, h->stream));
     h->stats.kernel_launches = 1;
@@ -733,7 +783,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     h->stats.children_evaluated = res[1];
     h->stats.parents_expanded = res[2];
     h->stats.alg_bytes = res[3];
-    h->stats.alg_ops = res[1] * (4 * (int64_t)W + 8);
+    h->stats.alg_ops = res[1] * 12; // counters-form lane-ops per child
     h->stats.d2h_bytes += 32 + 4 * (int64_t)n1;
     out->cost = res[0];
     out->children_evaluated = res[1];

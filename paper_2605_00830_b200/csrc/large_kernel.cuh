@@ -3,17 +3,35 @@
 // ("avoiding any host-device communication").  Used for n2 > 128 or very large K
 // (BASELINE configs[3]: n = 200-500, K = 1e4-1e5).
 //
-// Per level: the same Branch / Threshold / Count / Compact / Update steps as batch_kernel.cuh,
-// with the CTA replaced by the grid:
-//   A  every warp takes a contiguous range of parents; lanes take the g2 vertices u = lane + 32 s;
-//      the bit-packed g2 adjacency is held transposed in shared memory (word-major: lanes read
-//      consecutive banks); only the nonzero words of the parent's used mask are visited.  Rank
-//      codes go to HBM (1 byte per child), per-CTA histograms are merged with one global atomic per
-//      nonzero bin (the paper's local -> global ranking, made exact).
-//   T  every CTA reads the 256-bin global histogram and derives the same threshold (no extra sync).
-//   B  per-warp counts < t / == t; every CTA derives its warps' prefixes from the per-warp array.
-//   C  survivors are compacted in (parent, child) order; the next frontier rows are written with
-//      coalesced word copies; grid barriers separate the phases.
+// Node state in HBM (frontier k, row-major, double-buffered):
+//   ped[k] int32, used[k][W] uint32 (bit u: g2 vertex u is used), lambda map[k][n1s] (uint8, or
+//   uint16 when n2 > 254; all-ones = deleted), and the counters cnt[k][cs] (uint8, or uint16 when a
+//   g2 degree exceeds 255): cnt[k][u] = number of used g2 neighbours of u (the "counters"
+//   formulation of SURVEY.md §8(a) a1).  A child's counters are its parent's plus the adjacency row
+//   of its target, so the per-child O(W) popcount for cnt_p(u) becomes one byte load.
+//
+// Per level i (g1 vertex v_i):
+//   A  branch (Alg. 2): a warp per parent, lane l owns the targets
+//      u = 128 s + 4 l + b.  Child PED of the paper's incremental evaluation with the three
+//      implied-edge cases of P:103-116 regrouped as
+//          Delta(u)   = cv(i,u) + edel*d_i + eins*cnt_p(u) - (edel+eins)*cB_p(u) + esub*mis_p(u)
+//          Delta(DEL) = vdel + edel*d_i
+//      cB_p(u) = number of earlier g1 neighbours v_q of v_i whose image lambda_p(q) is adjacent to u
+//      (the paper's VFrom/VTo, reading C8).  Two ways to get it, chosen per level by cost:
+//        scatter: walk the neighbour lists of the images (CSR) and add into a per-warp array D[u]
+//                 (also yields mis_p for labelled edges);
+//        popcount: B_p as a bitmask, popc(adj2[u] & B_p) over the nonzero words of B_p.
+//      Each child becomes a one-byte rank code (PED - base + 1, saturated) in HBM; codes that can be
+//      selected (PED <= U_i, the bound of SURVEY.md §8(a) a2) go into a per-lane-column shared
+//      histogram (no intra-warp address conflicts), merged with one global atomic per nonzero bin.
+//   T  every CTA reads the global histogram and derives the same threshold t and tie quota r
+//      (replaces the paper's local/global ranking with atomics; exact, reading C12).
+//   B  per-warp counts of codes < t / == t (SWAR over 16-byte vectors).
+//   C1 survivors compacted in (parent, child) order (reading C13); word-level skip of code vectors
+//      without a survivor.
+//   C2 next frontier rows with coalesced warp-per-row copies (the paper's copy_kernel).
+// After the last level: insertion completion (reading C6) and argmin by (total, position)
+// (reading C10).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -24,21 +42,71 @@
 namespace fg {
 namespace cg = cooperative_groups;
 
+constexpr int LNT = 512; // threads per CTA of the large kernel
+
+template <typename MapT>
+struct MapDel { static constexpr int value = (int)(MapT)(~(MapT)0); };
+
+// Four consecutive counters (targets u..u+3) as one vector.
+template <typename CntT>
+struct Cnt4;
+template <>
+struct Cnt4<uint8_t> {
+    using V = uint32_t;
+    static __device__ __forceinline__ V load(const uint8_t *row, int u) { return *reinterpret_cast<const uint32_t *>(row + u); }
+    static __device__ __forceinline__ void store(uint8_t *row, int u, V v) { *reinterpret_cast<uint32_t *>(row + u) = v; }
+    static __device__ __forceinline__ int get(V v, int b) { return (int)((v >> (8 * b)) & 0xffu); }
+    // add bit b of nib to counter b (bits spread to bytes 0..3; no carries between the partial products)
+    static __device__ __forceinline__ V add_bits(V v, uint32_t nib) { return v + ((nib * 0x204081u) & 0x01010101u); }
+};
+template <>
+struct Cnt4<uint16_t> {
+    using V = uint2;
+    static __device__ __forceinline__ V load(const uint16_t *row, int u) { return *reinterpret_cast<const uint2 *>(row + u); }
+    static __device__ __forceinline__ void store(uint16_t *row, int u, V v) { *reinterpret_cast<uint2 *>(row + u) = v; }
+    static __device__ __forceinline__ int get(V v, int b) {
+        const uint32_t w = b < 2 ? v.x : v.y;
+        return (int)((w >> (16 * (b & 1))) & 0xffffu);
+    }
+    static __device__ __forceinline__ V add_bits(V v, uint32_t nib) {
+        v.x += (nib & 1u) | ((nib & 2u) << 15);
+        v.y += ((nib >> 2) & 1u) | ((nib & 8u) << 13);
+        return v;
+    }
+};
+
+// SWAR byte compares (unsigned, any byte values): bit 7 of each byte set where the predicate holds.
+__device__ __forceinline__ uint32_t bytes_lt(uint32_t x, uint32_t y) {
+    const uint32_t z = (x | 0x80808080u) - (y & 0x7f7f7f7fu); // bit 7: low 7 bits of x >= those of y
+    return ((~x & y) | (~(x ^ y) & ~z)) & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t bytes_eq(uint32_t x, uint32_t y) {
+    const uint32_t z = x ^ y;
+    return ~((((z & 0x7f7f7f7fu) + 0x7f7f7f7fu) | z)) & 0x80808080u;
+}
+
 struct LargeArgs {
     const uint8_t *blob;
     PairDesc pd;
     Costs c;
-    int32_t K, win, W, Wp; // Wp: words per transposed plane stride (n2 rounded up to 32)
-    int32_t n1s;           // lambda row stride in elements (multiple of 4 bytes)
-    int32_t adj_in_smem;
+    int32_t K, win, W;
+    int32_t cs, S;          // row stride of codes / counters (multiple of 128 >= n2 + 1); S = cs / 128
+    int32_t n1s;            // lambda row stride in elements (4-byte multiple)
+    int32_t n1r;            // staged P_i list capacity in shared memory (>= max d, multiple of 4)
+    int32_t adjT_in_smem;   // transposed adjacency adjT[W][cs] staged in shared memory
+    int32_t degw;           // ceil(mean g2 degree / 32): scatter-cost estimate
+    const int32_t *nptr;    // CSR of g2: [n2 + 1]
+    const uint32_t *nbr;    // [2 m2]: neighbour | (edge label id << 16)
+    const uint32_t *adjT;   // [W][cs]: bit (u' & 31) of adjT[w][u] = edge (u, 32 w + u')
     int32_t *ped[2];
-    uint32_t *used[2];
-    void *map[2];
-    uint8_t *codes; // [K * cs]
-    int32_t *sel_p, *sel_j;
-    int32_t *hist;          // [3][256]
+    uint32_t *used[2];      // [Kc][W]
+    void *cnt[2];           // [Kc][cs] CntT
+    void *map[2];           // [Kc][n1s] MapT
+    uint8_t *codes;         // [Kc][cs]
+    int32_t *sel_p, *sel_j; // survivors (parent position, child index; n2 = deletion)
+    int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
-    int32_t *lo;            // [n1 + 1] min survivor PED per level (init INT_MAX)
+    int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
     int32_t *wlt, *weq;     // [total warps]
     unsigned long long *best;
     int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes
@@ -46,25 +114,28 @@ struct LargeArgs {
     int64_t *levels_out;    // NULL or [3 n1]
 };
 
-template <typename MapT>
-struct MapDel { static constexpr int value = (int)(MapT)(~(MapT)0); };
+// Shared-memory bytes of the large kernel (must match the carve-up below).
+__host__ __device__ inline size_t large_smem_bytes(int cs, int n1r, int W, bool adjT_in_smem) {
+    return (size_t)256 * 32 * 4 + (size_t)2 * n1r * 4 + (size_t)(LNT / 32) * (64 + cs) * 4 +
+           (adjT_in_smem ? (size_t)W * cs * 4 : 0);
+}
 
-template <typename MapT, bool LAB>
-__device__ int large_child_scalar(const LargeArgs &a, int i, int d, const int32_t *pq, const int32_t *pl,
-                                  int pedp, const uint32_t *Up, const MapT *mrow, int j,
-                                  const uint32_t *adj2, const uint8_t *e2, int vl1i, const int32_t *vl2) {
+template <typename MapT, typename CntT, bool LAB>
+__device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, const int32_t *pl, int pedp,
+                                  const CntT *crow, const MapT *mrow, int j, const uint32_t *adj2,
+                                  const uint8_t *e2, int vl1i, const int32_t *vl2) {
     const Costs &c = a.c;
     const int n2 = a.pd.n2, W = a.W;
     if (j == n2) return pedp + c.vdel + c.edel * d;
-    int cv = (vl2[j] == vl1i) ? 0 : c.vsub;
-    int cnt = 0, cb = 0, mis = 0;
-    for (int w = 0; w < W; ++w) cnt += __popc(adj2[(int64_t)j * W + w] & Up[w]);
+    const int cv = (vl2[j] == vl1i) ? 0 : c.vsub;
+    const int cnt = (int)crow[j];
+    int cb = 0, mis = 0;
     for (int k = 0; k < d; ++k) {
-        int t = mrow[pq[k]];
+        const int t = mrow[pq[k]];
         if (t == MapDel<MapT>::value) continue;
         if (!LAB) cb += (adj2[(int64_t)j * W + (t >> 5)] >> (t & 31)) & 1u;
         else {
-            int e = e2[(int64_t)t * a.pd.n2p + j];
+            const int e = e2[(int64_t)t * a.pd.n2p + j];
             cb += (e != 0);
             mis += (e != 0) & (e != pl[k]);
         }
@@ -72,22 +143,21 @@ __device__ int large_child_scalar(const LargeArgs &a, int i, int d, const int32_
     return pedp + cv + c.edel * d + c.eins * cnt - (c.edel + c.eins) * cb + c.esub * mis;
 }
 
-template <typename MapT, bool LAB>
-__global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
+template <typename MapT, typename CntT, bool LAB>
+__global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
-    __shared__ int s_hist[256];
+    constexpr int NWB = LNT / 32;
     __shared__ int s_pre[2];
-    __shared__ int s_red[2][8];
+    __shared__ int s_red[2][NWB];
     __shared__ long long s_cnt;
     cg::grid_group grid = cg::this_grid();
+    using C4 = Cnt4<CntT>;
 
-    constexpr int NWB = 8; // warps per block (blockDim 256)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * NWB + wib, GW = gridDim.x * NWB;
     const Costs c = a.c;
     const PairDesc pd = a.pd;
-    const int n1 = pd.n1, n2 = pd.n2, W = a.W, Wp = a.Wp, K = a.K, win = a.win;
-    const int cs = (n2 + 1 + 3) & ~3;
+    const int n1 = pd.n1, n2 = pd.n2, W = a.W, K = a.K, win = a.win, cs = a.cs, S = a.S;
     constexpr int DELV = MapDel<MapT>::value;
     const int32_t *vl1 = reinterpret_cast<const int32_t *>(a.blob + pd.vl1);
     const int32_t *vl2 = reinterpret_cast<const int32_t *>(a.blob + pd.vl2);
@@ -97,39 +167,57 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
     const uint32_t *adj2 = reinterpret_cast<const uint32_t *>(a.blob + pd.adj2);
     const uint8_t *e2 = LAB ? (a.blob + pd.e2lab) : nullptr;
 
-    // shared: per-warp parent masks (U, B, nonzero word list) then the transposed adjacency
-    uint32_t *sU = reinterpret_cast<uint32_t *>(dsmem) + wib * 3 * W;
-    uint32_t *sB = sU + W;
-    int32_t *sNZ = reinterpret_cast<int32_t *>(sB + W);
-    uint32_t *adjT = reinterpret_cast<uint32_t *>(dsmem) + NWB * 3 * W;
-    if (a.adj_in_smem) {
-        for (int x = threadIdx.x; x < W * Wp; x += blockDim.x) {
-            const int w = x / Wp, u = x - w * Wp;
-            adjT[x] = (u < n2) ? adj2[(int64_t)u * W + w] : 0u;
-        }
+    // shared: per-lane-column histogram [256][32], the P_i list, per-warp (U, B, D[cs]), adjT
+    int *s_hist = reinterpret_cast<int *>(dsmem);
+    int32_t *s_pq = s_hist + 256 * 32;
+    int32_t *s_pl = s_pq + a.n1r;
+    uint32_t *wbase = reinterpret_cast<uint32_t *>(s_pl + a.n1r);
+    uint32_t *sU = wbase + wib * (64 + cs);
+    uint32_t *sB = sU + 32;
+    int *D = reinterpret_cast<int *>(sB + 32);
+    const uint32_t *adjT = a.adjT;
+    if (a.adjT_in_smem) {
+        uint32_t *t = wbase + NWB * (64 + cs);
+        for (int x = threadIdx.x; x < W * cs; x += LNT) t[x] = __ldg(a.adjT + x);
+        adjT = t;
     }
-    // root
+    for (int x = lane; x < cs; x += 32) D[x] = 0;
+    // root: lambda empty, nothing used, PED 0
     if (blockIdx.x == 0) {
         if (threadIdx.x == 0) a.ped[0][0] = 0;
-        for (int w = threadIdx.x; w < W; w += blockDim.x) a.used[0][w] = 0u;
+        for (int w = threadIdx.x; w < W; w += LNT) a.used[0][w] = 0u;
+        for (int u = threadIdx.x; u < cs; u += LNT) reinterpret_cast<CntT *>(a.cnt[0])[u] = 0;
     }
     block_sync();
-    __syncwarp();
-        grid.sync();
+    grid.sync();
 
-    int N = 1, lo = 0, cur = 0, ps = 0;
+    int N = 1, lo = 0, hi = 0, cur = 0, ps = 0;
     int64_t children = 0, parents = 0, algb = 0;
     for (int i = 0; i < n1; ++i) {
         const int32_t *Pped = a.ped[cur];
         const uint32_t *Pused = a.used[cur];
+        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[cur]);
         const MapT *Pmap = reinterpret_cast<const MapT *>(a.map[cur]);
         int32_t *Qped = a.ped[cur ^ 1];
         uint32_t *Qused = a.used[cur ^ 1];
+        CntT *Qcnt = reinterpret_cast<CntT *>(a.cnt[cur ^ 1]);
         MapT *Qmap = reinterpret_cast<MapT *>(a.map[cur ^ 1]);
-        const int pbeg = pptr[i], d = pptr[i + 1] - pbeg;
-        const int32_t *pq = pqg + pbeg, *pl = plg + pbeg;
-        const int vl1i = vl1[i];
+        const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
+        for (int k = threadIdx.x; k < d; k += LNT) {
+            s_pq[k] = __ldg(pqg + pbeg + k);
+            s_pl[k] = __ldg(plg + pbeg + k);
+        }
+        const int vl1i = __ldg(vl1 + i);
+        uint64_t mm = 0; // vertex-label mismatch of the lane's targets: bit 4 s + b for u = 128 s + 4 lane + b
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int u = 128 * s + 4 * lane + b;
+                if (u < n2 && __ldg(vl2 + u) != vl1i) mm |= 1ull << (4 * s + b);
+            }
         const int edd = c.edel * d, ee = c.edel + c.eins, pedDel = c.vdel + edd;
+        // cB by scatter over neighbour lists, or by popcount over the nonzero words of B_p (uniform choice)
+        const bool scatter = LAB || (d * a.degw * 8 < S * min(W, d) * 13);
         const int chunk = (N + GW - 1) / GW;
         const int p0 = min(N, gw * chunk), p1 = min(N, p0 + chunk);
         int base = lo, below = 0;
@@ -137,97 +225,150 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         int tcode = 0, rq = 0;
 
         for (;;) { // ---------------- A + T ----------------
-            for (int k = threadIdx.x; k < 256; k += blockDim.x) s_hist[k] = 0;
+            // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
+            // (each of the N parents has a deletion child <= U_i): their codes skip the histogram.
+            const int capc = (N >= K) ? max(0, min(win, hi + pedDel - base + 1)) : win;
+            for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
             if (threadIdx.x == 0) s_cnt = 0;
             if (blockIdx.x == 0)
-                for (int k = threadIdx.x; k < 256; k += blockDim.x) a.hist[((ps + 1) % 3) * 256 + k] = 0;
+                for (int k = threadIdx.x; k < 256; k += LNT) a.hist[((ps + 1) % 3) * 256 + k] = 0;
             block_sync();
             int wcount = 0;
             for (int p = p0; p < p1; ++p) {
                 const int pedp = Pped[p];
                 const MapT *mrow = Pmap + (int64_t)p * a.n1s;
-                for (int w = lane; w < W; w += 32) { sU[w] = Pused[(int64_t)p * W + w]; sB[w] = 0u; }
-                __syncwarp();
-                // B_p: images of the earlier g1 neighbours of v_i (PAPER.md:254 VFrom/VTo, reading C8)
-                if (!LAB)
-                    for (int k = lane; k < d; k += 32) {
-                        const int t = mrow[pq[k]];
-                        if (t != DELV) atomicOr(&sB[t >> 5], 1u << (t & 31));
-                    }
-                __syncwarp();
-                // nonzero words of U (B is a subset of U)
-                int nnz = 0;
-                for (int w0 = 0; w0 < W; w0 += 32) {
-                    const int w = w0 + lane;
-                    const bool nz = (w < W) && sU[w] != 0u;
-                    const unsigned m = __ballot_sync(FULL, nz);
-                    if (nz) sNZ[nnz + __popc(m & lanemask_lt())] = w;
-                    nnz += __popc(m);
+                int nused = 0;
+                for (int w = lane; w < W; w += 32) {
+                    const uint32_t uw = Pused[(int64_t)p * W + w];
+                    sU[w] = uw;
+                    nused += __popc(uw);
+                    if (!scatter) sB[w] = 0u;
                 }
+                nused = __reduce_add_sync(FULL, nused);
                 __syncwarp();
-                uint8_t *crow = a.codes + (int64_t)p * cs;
-                int nvalid = 1;
-                for (int u0 = 0; u0 < cs; u0 += 32) {
-                    const int u = u0 + lane;
-                    const bool sub = (u < n2) && !((sU[u >> 5] >> (u & 31)) & 1u);
-                    const bool del = (u == n2);
-                    int code = CODE_INVALID;
-                    int ped = 0;
-                    if (sub) {
-                        int cnt = 0, cb = 0, mis = 0;
-                        for (int z = 0; z < nnz; ++z) {
-                            const int w = sNZ[z];
-                            const uint32_t r = a.adj_in_smem ? adjT[(int64_t)w * Wp + u] : adj2[(int64_t)u * W + w];
-                            cnt += __popc(r & sU[w]);
-                            if (!LAB) cb += __popc(r & sB[w]);
-                        }
-                        if (LAB) {
-                            for (int k = 0; k < d; ++k) {
-                                const int t = mrow[pq[k]];
-                                if (t == DELV) continue;
-                                const int e = e2[(int64_t)t * pd.n2p + u];
-                                cb += (e != 0);
-                                mis += (e != 0) & (e != pl[k]);
+                uint32_t nzb = 0;
+                if (scatter) {
+                    // D[u] += 1 (+ 1 << 16 on a label mismatch) for every neighbour u of every image t_k
+                    for (int k0 = 0; k0 < d; k0 += 32) {
+                        const int kk = k0 + lane;
+                        const int tk = kk < d ? (int)mrow[s_pq[kk]] : DELV;
+                        const int lk = (LAB && kk < d) ? s_pl[kk] : 0;
+                        const int kn = min(32, d - k0);
+                        for (int z = 0; z < kn; ++z) {
+                            const int t = __shfl_sync(FULL, tk, z);
+                            if (t == DELV) continue;
+                            const int lz = LAB ? __shfl_sync(FULL, lk, z) : 0;
+                            const int e1 = __ldg(a.nptr + t + 1);
+                            for (int e = __ldg(a.nptr + t) + lane; e < e1; e += 32) {
+                                const uint32_t v = __ldg(a.nbr + e);
+                                atomicAdd(&D[v & 0xffffu], (LAB && (int)(v >> 16) != lz) ? 0x10001 : 1);
                             }
                         }
-                        ped = pedp + ((vl2[u] == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - ee * cb + c.esub * mis;
-                    } else if (del) {
-                        ped = pedp + pedDel;
                     }
-                    if (sub || del) {
-                        const int x = ped - base + 1;
-                        code = x < 0 ? 0 : (x > win ? win + 1 : x);
-                        if (code >= 1 && code <= win) atomicAdd(&s_hist[code], 1);
+                } else {
+                    for (int k = lane; k < d; k += 32) {
+                        const int t = mrow[s_pq[k]];
+                        if (t != DELV) atomicOr(&sB[t >> 5], 1u << (t & 31));
                     }
-                    if (u < cs) crow[u] = (uint8_t)code;
-                    nvalid += __popc(__ballot_sync(FULL, sub));
+                    __syncwarp();
+                    nzb = __ballot_sync(FULL, lane < W && sB[lane] != 0u);
                 }
-                wcount += nvalid;
+                __syncwarp();
+                const int pb = pedp - base + 1 + edd;
+                uint8_t *crow = a.codes + (int64_t)p * cs;
+                const CntT *cr = Pcnt + (int64_t)p * cs;
+                for (int s = 0; s < S; ++s) {
+                    const int u0 = 128 * s + 4 * lane;
+                    const typename C4::V cv = C4::load(cr, u0);
+                    const uint32_t ub = (sU[min(u0 >> 5, 31)] >> (u0 & 31)) & 0xfu;
+                    int cb[4] = {0, 0, 0, 0}, ms[4] = {0, 0, 0, 0};
+                    if (scatter) {
+                        int4 *dp = reinterpret_cast<int4 *>(D + u0);
+                        const int4 dv = *dp;
+                        *dp = make_int4(0, 0, 0, 0);
+                        cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
+                        if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
+                    } else {
+                        uint32_t m = nzb;
+                        while (m) {
+                            const int w = __ffs(m) - 1;
+                            m &= m - 1;
+                            const uint4 av = *reinterpret_cast<const uint4 *>(adjT + (int64_t)w * cs + u0);
+                            const uint32_t bw = sB[w];
+                            cb[0] += __popc(av.x & bw); cb[1] += __popc(av.y & bw);
+                            cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
+                        }
+                    }
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int u = u0 + b;
+                        int code;
+                        if (u < n2 && !((ub >> b) & 1u)) {
+                            const int x = pb + (int)((mm >> (4 * s + b)) & 1ull) * c.vsub + c.eins * C4::get(cv, b) -
+                                          ee * cb[b] + (LAB ? c.esub * ms[b] : 0);
+                            code = min(max(x, 0), win + 1);
+                        } else if (u == n2) {
+                            code = rank_code(pedp + pedDel, base, win); // deletion child (reading C5)
+                        } else {
+                            code = CODE_INVALID;
+                        }
+                        if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
+                        word |= (uint32_t)code << (8 * b);
+                    }
+                    *reinterpret_cast<uint32_t *>(crow + u0) = word;
+                }
+                wcount += n2 - nused + 1;
                 __syncwarp();
             }
             if (first && lane == 0) atomicAdd((unsigned long long *)&s_cnt, (unsigned long long)wcount);
             block_sync();
             int *gh = a.hist + (ps % 3) * 256;
-            for (int k = threadIdx.x; k < 256; k += blockDim.x)
-                if (s_hist[k]) atomicAdd(&gh[k], s_hist[k]);
+            for (int bin = threadIdx.x; bin < 256; bin += LNT) {
+                int v = 0;
+#pragma unroll 8
+                for (int l = 0; l < 32; ++l) v += s_hist[bin * 32 + ((l + bin) & 31)];
+                if (v) atomicAdd(&gh[bin], v);
+            }
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
             block_sync();
-        grid.sync();
-            // T: every CTA derives the same threshold
+            grid.sync();
+            // T: every CTA derives the same threshold from the global histogram
             const int64_t ci = a.ci[i];
             keepall = (ci <= K);
             bool retry = false;
             if (!keepall) {
-                // warp 0 of each block scans; broadcast via smem
-                if (threadIdx.x == 0) {
-                    int cum = below, t = 0;
-                    for (int b = 1; b <= win; ++b) {
-                        const int hv = gh[b];
-                        if (cum + hv >= K) { t = b; break; }
-                        cum += hv;
+                if (wib == 0) {
+                    int hv[8], sum = 0;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const int bb = 8 * lane + x + 1; // codes 1..256
+                        hv[x] = (bb <= capc) ? gh[bb] : 0;
+                        sum += hv[x];
                     }
-                    s_pre[0] = t;
-                    s_pre[1] = t ? (K - cum) : (cum - below);
+                    int incl = sum;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const unsigned hm = __ballot_sync(FULL, below + incl >= K);
+                    if (hm) {
+                        const int L = __ffs(hm) - 1;
+                        if (lane == L) {
+                            int c2 = below + incl - sum, tc = 0, rr = 0;
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) {
+                                if (tc == 0 && c2 + hv[x] >= K) { tc = 8 * lane + x + 1; rr = K - c2; }
+                                c2 += hv[x];
+                            }
+                            s_pre[0] = tc;
+                            s_pre[1] = rr;
+                        }
+                    } else if (lane == 31) {
+                        s_pre[0] = 0;
+                        s_pre[1] = incl; // every code of the window lies below the K-th smallest
+                    }
                 }
                 block_sync();
                 tcode = s_pre[0];
@@ -239,22 +380,27 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             ps++;
             first = false;
             if (!retry) break;
-            base += win;
+            base += win; // the K-th smallest PED lies beyond the window: slide it (codes 0 = kept)
         }
 
-        // ---------------- B: per-warp counts ----------------
+        // ---------------- B: per-warp counts of codes < t and == t ----------------
+        const uint4 *cvec = reinterpret_cast<const uint4 *>(a.codes + (int64_t)p0 * cs);
+        const int nvec = (p1 - p0) * cs / 16;
+        const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
+        const uint32_t inv4 = (uint32_t)CODE_INVALID * 0x01010101u;
+        auto masks = [&](uint32_t v, uint32_t &mlt, uint32_t &meq) {
+            if (keepall) { mlt = ~bytes_eq(v, inv4) & 0x80808080u; meq = 0u; }
+            else { mlt = bytes_lt(v, t4); meq = bytes_eq(v, t4); }
+        };
         {
             int lt = 0, eq = 0;
-            const uint32_t *cw = reinterpret_cast<const uint32_t *>(a.codes + (int64_t)p0 * cs);
-            const int64_t nwords = (int64_t)(p1 - p0) * cs / 4;
-            const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
-            for (int64_t x = lane; x < nwords; x += 32) {
-                const uint32_t v = cw[x];
-                if (keepall) lt += __popc(__vcmpne4(v, 0xffffffffu)) >> 3;
-                else {
-                    lt += __popc(__vcmpltu4(v, t4)) >> 3;
-                    eq += __popc(__vcmpeq4(v, t4)) >> 3;
-                }
+            for (int x = lane; x < nvec; x += 32) {
+                const uint4 v = cvec[x];
+                uint32_t m0, e0;
+                masks(v.x, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                masks(v.y, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                masks(v.z, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                masks(v.w, m0, e0); lt += __popc(m0); eq += __popc(e0);
             }
             lt = __reduce_add_sync(FULL, lt);
             eq = __reduce_add_sync(FULL, eq);
@@ -267,7 +413,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         {
             int slt = 0, seq = 0;
             const int first_w = blockIdx.x * NWB;
-            for (int g = threadIdx.x; g < first_w; g += blockDim.x) { slt += a.wlt[g]; seq += a.weq[g]; }
+            for (int g = threadIdx.x; g < first_w; g += LNT) { slt += a.wlt[g]; seq += a.weq[g]; }
             slt = __reduce_add_sync(FULL, slt);
             seq = __reduce_add_sync(FULL, seq);
             if (lane == 0) { s_red[0][wib] = slt; s_red[1][wib] = seq; }
@@ -278,28 +424,51 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         for (int w = blockIdx.x * NWB; w < gw; ++w) { ltpre += a.wlt[w]; eqpre += a.weq[w]; }
         const int Nn = keepall ? (int)a.ci[i] : K;
 
-        // ---------------- C1: compact survivors ----------------
+        // ---------------- C1: compact survivors in (parent, child) order ----------------
         {
             int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
-            const unsigned lmask = lanemask_lt();
-            for (int p = p0; p < p1; ++p) {
-                const uint8_t *crow = a.codes + (int64_t)p * cs;
-                for (int u0 = 0; u0 < cs; u0 += 32) {
-                    const int u = u0 + lane;
-                    const int code = (u < cs) ? crow[u] : CODE_INVALID;
-                    const bool lt = keepall ? (code != CODE_INVALID) : (code < tcode);
-                    const bool eq = !keepall && (code == tcode);
-                    const unsigned eqm = __ballot_sync(FULL, eq);
-                    const bool keep = lt || (eq && (eq_seen + __popc(eqm & lmask)) < rq);
-                    const unsigned km = __ballot_sync(FULL, keep);
-                    if (keep) {
-                        const int pos = out + __popc(km & lmask);
-                        a.sel_p[pos] = p;
-                        a.sel_j[pos] = u;
-                    }
-                    out += __popc(km);
-                    eq_seen += __popc(eqm);
+            for (int x0 = 0; x0 < nvec; x0 += 32) {
+                const int x = x0 + lane;
+                const uint4 v = x < nvec ? cvec[x] : make_uint4(inv4, inv4, inv4, inv4);
+                uint32_t ml[4], me[4];
+                masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
+                masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
+                const int nlt = __popc(ml[0]) + __popc(ml[1]) + __popc(ml[2]) + __popc(ml[3]);
+                const int neq = __popc(me[0]) + __popc(me[1]) + __popc(me[2]) + __popc(me[3]);
+                if (!__any_sync(FULL, (nlt | neq) != 0)) continue;
+                int einc = neq;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, einc, o);
+                    if (lane >= o) einc += y;
                 }
+                const int adm = min(neq, max(0, rq - (eq_seen + einc - neq))); // ties admitted in code order
+                const int keep = nlt + adm;
+                int kinc = keep;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, kinc, o);
+                    if (lane >= o) kinc += y;
+                }
+                int pos = out + kinc - keep, ecnt = 0;
+                if (keep) {
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        uint32_t m = ml[w], e = me[w];
+                        while (e && ecnt < adm) { const uint32_t lowb = e & (0u - e); m |= lowb; e ^= lowb; ++ecnt; }
+                        while (m) {
+                            const int by = (__ffs(m) - 1) >> 3;
+                            m &= m - 1;
+                            const int64_t g = (int64_t)p0 * cs + 16 * (int64_t)x + 4 * w + by;
+                            const int p = (int)(g / cs);
+                            a.sel_p[pos] = p;
+                            a.sel_j[pos] = (int)(g - (int64_t)p * cs);
+                            ++pos;
+                        }
+                    }
+                }
+                out += __shfl_sync(FULL, kinc, 31);
+                eq_seen += __shfl_sync(FULL, einc, 31);
             }
         }
         if (blockIdx.x == 0 && threadIdx.x == 0 && a.levels_out) {
@@ -310,43 +479,52 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         block_sync();
         grid.sync();
 
-        // ---------------- C2: next frontier ----------------
-        const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
-        int mylo = 0x7fffffff;
-        for (int k = gtid; k < Nn; k += gthreads) {
-            const int p = a.sel_p[k], j = a.sel_j[k];
-            const int code = a.codes[(int64_t)p * cs + j];
-            int ped;
-            if (code >= 1 && code <= win) ped = base + code - 1;
-            else
-                ped = large_child_scalar<MapT, LAB>(a, i, d, pq, pl, Pped[p], Pused + (int64_t)p * W,
-                                                    Pmap + (int64_t)p * a.n1s, j, adj2, e2, vl1i, vl2);
-            Qped[k] = ped;
-            mylo = min(mylo, ped);
-        }
-        mylo = __reduce_min_sync(FULL, mylo);
-        if (lane == 0 && mylo != 0x7fffffff) atomicMin(&a.lo[i + 1], mylo);
-        for (int64_t x = gtid; x < (int64_t)Nn * W; x += gthreads) {
-            const int k = (int)(x / W), w = (int)(x - (int64_t)k * W);
-            const int p = a.sel_p[k], j = a.sel_j[k];
-            uint32_t v = Pused[(int64_t)p * W + w];
-            if (j < n2 && (j >> 5) == w) v |= 1u << (j & 31);
-            Qused[x] = v;
-        }
+        // ---------------- C2: next frontier, a warp per survivor row ----------------
         {
-            constexpr int EPW = 4 / sizeof(MapT); // map entries per 32-bit word
+            int mylo = 0x7fffffff, myhi = (int)0x80000000;
+            constexpr int EPW = 4 / sizeof(MapT); // lambda entries per 32-bit word
             const int wpr = (i + EPW) / EPW, hw = i / EPW, sh = (i % EPW) * 8 * (int)sizeof(MapT);
             const int rowwords = a.n1s * (int)sizeof(MapT) / 4;
             const uint32_t emask = (sizeof(MapT) == 1) ? 0xffu : 0xffffu;
-            for (int64_t x = gtid; x < (int64_t)Nn * wpr; x += gthreads) {
-                const int k = (int)(x / wpr), w = (int)(x - (int64_t)k * wpr);
+            for (int k = gw; k < Nn; k += GW) {
                 const int p = a.sel_p[k], j = a.sel_j[k];
-                uint32_t word = reinterpret_cast<const uint32_t *>(Pmap)[(int64_t)p * rowwords + w];
-                if (w == hw) {
-                    const uint32_t e = (j == n2) ? (uint32_t)DELV : (uint32_t)j;
-                    word = (word & ~(emask << sh)) | (e << sh);
+                const CntT *pr = Pcnt + (int64_t)p * cs;
+                if (lane == 0) {
+                    const int code = a.codes[(int64_t)p * cs + j];
+                    int ped;
+                    if (code >= 1 && code <= win) ped = base + code - 1;
+                    else // saturated code: recompute (rare)
+                        ped = large_child_scalar<MapT, CntT, LAB>(a, d, s_pq, s_pl, Pped[p], pr, Pmap + (int64_t)p * a.n1s,
+                                                                  j, adj2, e2, vl1i, vl2);
+                    Qped[k] = ped;
+                    mylo = min(mylo, ped);
+                    myhi = max(myhi, ped);
                 }
-                reinterpret_cast<uint32_t *>(Qmap)[(int64_t)k * rowwords + w] = word;
+                for (int w = lane; w < W; w += 32) {
+                    uint32_t v = Pused[(int64_t)p * W + w];
+                    if (j < n2 && (j >> 5) == w) v |= 1u << (j & 31);
+                    Qused[(int64_t)k * W + w] = v;
+                }
+                CntT *qr = Qcnt + (int64_t)k * cs;
+                for (int u0 = 4 * lane; u0 < cs; u0 += 128) {
+                    typename C4::V v = C4::load(pr, u0);
+                    if (j < n2 && (u0 >> 5) < W) v = C4::add_bits(v, (__ldg(adj2 + (int64_t)j * W + (u0 >> 5)) >> (u0 & 31)) & 0xfu);
+                    C4::store(qr, u0, v);
+                }
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(Pmap) + (int64_t)p * rowwords;
+                uint32_t *dst = reinterpret_cast<uint32_t *>(Qmap) + (int64_t)k * rowwords;
+                for (int w = lane; w < wpr; w += 32) {
+                    uint32_t word = src[w];
+                    if (w == hw) {
+                        const uint32_t e = (j == n2) ? (uint32_t)DELV : (uint32_t)j;
+                        word = (word & ~(emask << sh)) | (e << sh);
+                    }
+                    dst[w] = word;
+                }
+            }
+            if (lane == 0 && mylo != 0x7fffffff) {
+                atomicMin(&a.lo[i + 1], mylo);
+                atomicMax(&a.hi[i + 1], myhi);
             }
         }
         parents += N;
@@ -355,6 +533,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
         grid.sync();
         N = Nn;
         lo = a.lo[i + 1];
+        hi = a.hi[i + 1];
         cur ^= 1;
     }
 
@@ -362,15 +541,14 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
     {
         const int32_t *Pped = a.ped[cur];
         const uint32_t *Pused = a.used[cur];
+        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[cur]);
         for (int k = gw; k < N; k += GW) { // warp per survivor
             int usedc = 0, e2u2 = 0;
             for (int w = lane; w < W; w += 32) usedc += __popc(Pused[(int64_t)k * W + w]);
-            for (int u = lane; u < n2; u += 32) {
-                if (!((Pused[(int64_t)k * W + (u >> 5)] >> (u & 31)) & 1u)) continue;
-                for (int w = 0; w < W; ++w) e2u2 += __popc(adj2[(int64_t)u * W + w] & Pused[(int64_t)k * W + w]);
-            }
+            for (int u = lane; u < n2; u += 32)
+                if ((Pused[(int64_t)k * W + (u >> 5)] >> (u & 31)) & 1u) e2u2 += (int)Pcnt[(int64_t)k * cs + u];
             usedc = __reduce_add_sync(FULL, usedc);
-            e2u2 = __reduce_add_sync(FULL, e2u2);
+            e2u2 = __reduce_add_sync(FULL, e2u2); // every edge among used vertices counted from both ends
             if (lane == 0) {
                 const int64_t total = (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) +
                                       (int64_t)c.eins * (pd.m2 - e2u2 / 2);
@@ -383,7 +561,7 @@ __global__ void __launch_bounds__(256) kbest_large_kernel(const LargeArgs a) {
             const unsigned long long best = *a.best;
             const int kb = (int)(best & 0xffffffffull);
             const MapT *row = reinterpret_cast<const MapT *>(a.map[cur]) + (int64_t)kb * a.n1s;
-            for (int q = threadIdx.x; q < n1; q += blockDim.x) {
+            for (int q = threadIdx.x; q < n1; q += LNT) {
                 const int t = row[q];
                 a.map_out[q] = (t == DELV) ? -1 : t;
             }

@@ -185,9 +185,9 @@ def test_large_path_small_pairs_forced(fg, oracle):
     hw.close()
 
 
-@pytest.mark.parametrize("n,p,K", [(150, 0.2, 2000), (260, 0.05, 1000), (300, 0.1, 500)])
+@pytest.mark.parametrize("n,p,K", [(150, 0.2, 2000), (260, 0.05, 1000), (300, 0.1, 500), (300, 0.92, 48)])
 def test_large_pairs(fg, handle, oracle, n, p, K):
-    """n2 > 128 (uint8 and uint16 lambda rows) against the oracle."""
+    """n2 > 128 (uint8 and uint16 lambda rows; p=0.92 gives g2 degrees > 255, i.e. uint16 counters) against the oracle."""
     g1, g2 = synth.large_pair(n, p, seed=9)
     r = handle.solve_pair(g1, g2, COSTS["setting1"], K, levels=True)
     o = oracle.kbest(g1, g2, COSTS["setting1"], K, levels=True)
