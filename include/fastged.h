@@ -127,6 +127,10 @@ typedef struct {
                                      lambda entry                                    */
     int64_t alg_ops;              /* algorithmic integer lane-ops of the branch step: sum over children of
                                      4 W + 8, W = ceil(n2 / 32) words per bit row     */
+    float phase_ms[5];            /* whole-GPU (large-pair) kernel only: time in its phases A+T (branch,
+                                     rank), B (count), C1 (compact), C2 (update), finalize; 0 otherwise */
+    int64_t hist_children;        /* whole-GPU kernel: children whose rank code entered the histogram
+                                     (PED <= U_i bound); 0 otherwise           */
 } fastged_stats_t;
 
 /* Create a handle.  Returns FASTGED_ERR_CUDA if the device cannot be used, FASTGED_ERR_NCCL if the

@@ -63,7 +63,8 @@ class StatsT(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("device_ms", C.c_float), ("branch_ms", C.c_float),
                 ("branch_launches", C.c_int64), ("children_evaluated", C.c_int64),
                 ("parents_expanded", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("alg_bytes", C.c_int64), ("alg_ops", C.c_int64)]
+                ("alg_bytes", C.c_int64), ("alg_ops", C.c_int64), ("phase_ms", C.c_float * 5),
+                ("hist_children", C.c_int64)]
 
 
 _lib = None
@@ -215,7 +216,7 @@ class Handle:
     def stats(self) -> dict:
         s = StatsT()
         self._check(self._L.fastged_get_stats(self._h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in StatsT._fields_}
+        return {k: (list(getattr(s, k)) if k == "phase_ms" else getattr(s, k)) for k, _ in StatsT._fields_}
 
     def upload(self, packed: PackedGraphs, pair_a, pair_b) -> "DeviceBatch":
         return DeviceBatch(self, packed, pair_a, pair_b)

@@ -692,8 +692,21 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
         for (int x : dd) dmax = std::max(dmax, x);
     }
     const int n1r = std::max(4, (dmax + 3) & ~3);
-    bool adjT_in_smem = fg::large_smem_bytes(cs, n1r, W, true) <= (size_t)h->smem_optin;
-    const size_t smem = fg::large_smem_bytes(cs, n1r, W, adjT_in_smem);
+    // shared-memory staging: the CSR when the scatter form is likely (sparse g2), the transposed
+    // rows otherwise; both when they fit; fewer branching warps per CTA only as a last resort
+    const int nnbr = 2 * g2->m;
+    const bool sparse = (n2 ? 2 * g2->m / n2 : 0) <= 32;
+    bool csr_in_smem = false, adjT_in_smem = false;
+    int nwa = fg::LNT / 32;
+    auto fits = [&](bool at, bool cr, int nw) {
+        return fg::large_smem_bytes(cs, csz, n1s, esz, nw, n1r, W, n2, nnbr, at, cr) <= (size_t)h->smem_optin;
+    };
+    if (fits(true, true, nwa)) adjT_in_smem = csr_in_smem = true;
+    else if (sparse && fits(false, true, nwa)) csr_in_smem = true;
+    else if (fits(true, false, nwa)) adjT_in_smem = true;
+    else if (fits(false, true, nwa)) csr_in_smem = true;
+    while (nwa > 1 && !fits(adjT_in_smem, csr_in_smem, nwa)) nwa--;
+    const size_t smem = fg::large_smem_bytes(cs, csz, n1s, esz, nwa, n1r, W, n2, nnbr, adjT_in_smem, csr_in_smem);
     if (smem > (size_t)h->smem_optin) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
     void *kfn = nullptr;
 #define LK(M, C, L) (void *)fg::kbest_large_kernel<M, C, L>
@@ -706,7 +719,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, fg::LNT, smem));
     if (occ < 1) fail(FASTGED_ERR_CAPACITY, "large-mode kernel does not fit on an SM (smem %zu)", smem);
-    occ = std::min(occ, 2);
+    occ = 1; // one CTA per SM (the grid barrier cost grows with the CTA count)
     const int grid = occ * h->sms;
     const int GW = grid * (fg::LNT / 32);
     // device buffers
@@ -717,9 +730,10 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     size_t o_cnt0 = take((size_t)csz * cs * Kc), o_cnt1 = take((size_t)csz * cs * Kc);
     size_t o_map0 = take((size_t)esz * n1s * Kc), o_map1 = take((size_t)esz * n1s * Kc);
     size_t o_codes = take((size_t)Kc * cs), o_selp = take(4 * (size_t)Kc), o_selj = take(4 * (size_t)Kc);
+    size_t o_selped = take(4 * (size_t)Kc);
     size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1));
     size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
-    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(32);
+    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(80);
     size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
     CK(h->lbuf.reserve(off));
     uint8_t *B = (uint8_t *)h->lbuf.p;
@@ -741,6 +755,9 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.n1s = n1s;
     a.n1r = n1r;
     a.adjT_in_smem = adjT_in_smem ? 1 : 0;
+    a.csr_in_smem = csr_in_smem ? 1 : 0;
+    a.csz = csz;
+    a.nwa = nwa;
     a.degw = std::max(1, (n2 ? (2 * g2->m + n2 - 1) / n2 : 0) + 31) / 32;
     a.nptr = (const int32_t *)(dblob + o_nptr);
     a.nbr = (const uint32_t *)(dblob + o_nbr);
@@ -750,7 +767,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.cnt[0] = B + o_cnt0; a.cnt[1] = B + o_cnt1;
     a.map[0] = B + o_map0; a.map[1] = B + o_map1;
     a.codes = B + o_codes;
-    a.sel_p = (int32_t *)(B + o_selp); a.sel_j = (int32_t *)(B + o_selj);
+    a.sel_p = (int32_t *)(B + o_selp); a.sel_j = (int32_t *)(B + o_selj); a.sel_ped = (int32_t *)(B + o_selped);
     a.hist = (int32_t *)(B + o_hist);
     a.ci = (int64_t *)(B + o_ci);
     a.lo = (int32_t *)(B + o_lo);
@@ -769,8 +786,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     CK(cudaEventRecord(e1, h->stream));
     CK(cudaEventRecord(h->ev_end, h->stream));
     h->stats.kernel_launches = 1;
-    int64_t res[4];
-    CK(cudaMemcpyAsync(res, a.out, 32, cudaMemcpyDeviceToHost, h->stream));
+    int64_t res[10];
+    CK(cudaMemcpyAsync(res, a.out, 80, cudaMemcpyDeviceToHost, h->stream));
     if (n1) CK(cudaMemcpyAsync(out->mapping, a.map_out, 4 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
     if (levels_out && n1) CK(cudaMemcpyAsync(levels_out, a.levels_out, 24 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -784,6 +801,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     h->stats.parents_expanded = res[2];
     h->stats.alg_bytes = res[3];
     h->stats.alg_ops = res[1] * 12; // counters-form lane-ops per child
+    for (int x = 0; x < 5; ++x) h->stats.phase_ms[x] = (float)(res[4 + x] * 1e-6);
+    h->stats.hist_children = res[9];
     h->stats.d2h_bytes += 32 + 4 * (int64_t)n1;
     out->cost = res[0];
     out->children_evaluated = res[1];

@@ -3,15 +3,19 @@
 // ("avoiding any host-device communication").  Used for n2 > 128 or very large K
 // (BASELINE configs[3]: n = 200-500, K = 1e4-1e5).
 //
-// Node state in HBM (frontier k, row-major, double-buffered):
-//   ped[k] int32, used[k][W] uint32 (bit u: g2 vertex u is used), lambda map[k][n1s] (uint8, or
-//   uint16 when n2 > 254; all-ones = deleted), and the counters cnt[k][cs] (uint8, or uint16 when a
-//   g2 degree exceeds 255): cnt[k][u] = number of used g2 neighbours of u (the "counters"
-//   formulation of SURVEY.md §8(a) a1).  A child's counters are its parent's plus the adjacency row
-//   of its target, so the per-child O(W) popcount for cnt_p(u) becomes one byte load.
+// Node state in HBM (row-major, double-buffered by level parity): used[k][W] uint32 (bit u: g2
+//   vertex u is used), lambda map[k][n1s] (uint8, or uint16 when n2 > 254; all-ones = deleted), and
+//   the counters cnt[k][cs] (uint8, or uint16 when a g2 degree exceeds 255): cnt[k][u] = number of
+//   used g2 neighbours of u (the "counters" formulation of SURVEY.md §8(a) a1).  A child's counters
+//   are its parent's plus the adjacency row of its target, so the per-child O(W) popcount for
+//   cnt_p(u) becomes one byte load.  The survivors of a level are kept as descriptors
+//   sel[k] = (parent position p, target j, PED); their rows are materialised by the next level's
+//   branch step, which reads the parent's row once and both writes the child's row and expands it
+//   (the paper's update/copy_kernel, fused into the following branch).
 //
 // Per level i (g1 vertex v_i):
-//   A  branch (Alg. 2): a warp per parent, lane l owns the targets
+//   A  materialise + branch (Alg. 2): a warp per parent (taken
+//      dynamically inside the CTA's range, rows prefetched with cp.async), lane l owns the targets
 //      u = 128 s + 4 l + b.  Child PED of the paper's incremental evaluation with the three
 //      implied-edge cases of P:103-116 regrouped as
 //          Delta(u)   = cv(i,u) + edel*d_i + eins*cnt_p(u) - (edel+eins)*cB_p(u) + esub*mis_p(u)
@@ -27,9 +31,8 @@
 //   T  every CTA reads the global histogram and derives the same threshold t and tie quota r
 //      (replaces the paper's local/global ranking with atomics; exact, reading C12).
 //   B  per-warp counts of codes < t / == t (SWAR over 16-byte vectors).
-//   C1 survivors compacted in (parent, child) order (reading C13); word-level skip of code vectors
-//      without a survivor.
-//   C2 next frontier rows with coalesced warp-per-row copies (the paper's copy_kernel).
+//   C1 survivors compacted in (parent, child) order (reading C13) into sel with their PEDs; 16-byte
+//      code vectors without a survivor are skipped.
 // After the last level: insertion completion (reading C6) and argmin by (total, position)
 // (reading C10).
 #pragma once
@@ -42,7 +45,19 @@
 namespace fg {
 namespace cg = cooperative_groups;
 
-constexpr int LNT = 512; // threads per CTA of the large kernel
+constexpr int LNT = 512; // threads per CTA of the large kernel (one CTA per SM)
+constexpr int LPF = 2;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cpa4(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa16(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <typename MapT>
 struct MapDel { static constexpr int value = (int)(MapT)(~(MapT)0); };
@@ -93,33 +108,48 @@ struct LargeArgs {
     int32_t cs, S;          // row stride of codes / counters (multiple of 128 >= n2 + 1); S = cs / 128
     int32_t n1s;            // lambda row stride in elements (4-byte multiple)
     int32_t n1r;            // staged P_i list capacity in shared memory (>= max d, multiple of 4)
+    int32_t nwa;            // warps per CTA with a branch region (shared-memory bound, <= LNT / 32)
     int32_t adjT_in_smem;   // transposed adjacency adjT[W][cs] staged in shared memory
+    int32_t csr_in_smem;    // CSR (nptr, nbr) staged in shared memory
+    int32_t csz;            // bytes per counter (1 or 2)
     int32_t degw;           // ceil(mean g2 degree / 32): scatter-cost estimate
     const int32_t *nptr;    // CSR of g2: [n2 + 1]
     const uint32_t *nbr;    // [2 m2]: neighbour | (edge label id << 16)
     const uint32_t *adjT;   // [W][cs]: bit (u' & 31) of adjT[w][u] = edge (u, 32 w + u')
-    int32_t *ped[2];
-    uint32_t *used[2];      // [Kc][W]
+    int32_t *ped[2];        // [Kc]      PED of the nodes of a level
+    uint32_t *used[2];      // [Kc][W]   rows of the nodes of level L live in buffer L & 1
     void *cnt[2];           // [Kc][cs] CntT
     void *map[2];           // [Kc][n1s] MapT
     uint8_t *codes;         // [Kc][cs]
-    int32_t *sel_p, *sel_j; // survivors (parent position, child index; n2 = deletion)
+    int32_t *sel_p, *sel_j, *sel_ped; // survivors: parent position, target (n2 = deletion, -1 = root), PED
     int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
     int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
     int32_t *wlt, *weq;     // [total warps]
     unsigned long long *best;
-    int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes
+    int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes,
+                            // [4..8] ns in phases A+T, B, C1, -, finalize (CTA 0's clock),
+                            // [9] children that entered the rank histogram
     int32_t *map_out;       // [n1]
     int64_t *levels_out;    // NULL or [3 n1]
 };
 
-// Shared-memory bytes of the large kernel (must match the carve-up below).
-__host__ __device__ inline size_t large_smem_bytes(int cs, int n1r, int W, bool adjT_in_smem) {
-    return (size_t)256 * 32 * 4 + (size_t)2 * n1r * 4 + (size_t)(LNT / 32) * (64 + cs) * 4 +
-           (adjT_in_smem ? (size_t)W * cs * 4 : 0);
+// Per-warp shared region (32-bit words): sB[32], D[cs], then LPF prefetch buffers of
+// counters[cs * csz / 4], used[32], lambda row [n1s * esz / 4], descriptor (k, p, j, ped)[4].
+__host__ __device__ inline int large_pf_words(int cs, int csz, int n1s, int esz) { // multiple of 4 (16-byte copies)
+    return ((cs * csz / 4 + 32 + n1s * esz / 4 + 4) + 3) & ~3;
+}
+__host__ __device__ inline int large_warp_words(int cs, int csz, int n1s, int esz) {
+    return 32 + cs + LPF * large_pf_words(cs, csz, n1s, esz);
+}
+// Shared-memory bytes of the large kernel (must match the carve-up in the kernel).
+__host__ __device__ inline size_t large_smem_bytes(int cs, int csz, int n1s, int esz, int nwa, int n1r, int W, int n2,
+                                                   int nnbr, bool adjT_in_smem, bool csr_in_smem) {
+    return (size_t)256 * 32 * 4 + (size_t)2 * n1r * 4 + (size_t)nwa * large_warp_words(cs, csz, n1s, esz) * 4 +
+           (adjT_in_smem ? (size_t)W * cs * 4 : 0) + (csr_in_smem ? (size_t)4 * (((n2 + 4) & ~3) + nnbr) : 0);
 }
 
+// PED of child (parent row k, target j) from scratch over P_i (rare: saturated rank codes).
 template <typename MapT, typename CntT, bool LAB>
 __device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, const int32_t *pl, int pedp,
                                   const CntT *crow, const MapT *mrow, int j, const uint32_t *adj2,
@@ -144,12 +174,14 @@ __device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, 
 }
 
 template <typename MapT, typename CntT, bool LAB>
-__global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) {
+__global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     constexpr int NWB = LNT / 32;
+    constexpr int ESZ = (int)sizeof(MapT);
     __shared__ int s_pre[2];
     __shared__ int s_red[2][NWB];
     __shared__ long long s_cnt;
+    __shared__ int s_next; // A: next parent of this CTA's range (warps take parents dynamically)
     cg::grid_group grid = cg::this_grid();
     using C4 = Cnt4<CntT>;
 
@@ -166,42 +198,71 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
     const int32_t *plg = reinterpret_cast<const int32_t *>(a.blob + pd.pl);
     const uint32_t *adj2 = reinterpret_cast<const uint32_t *>(a.blob + pd.adj2);
     const uint8_t *e2 = LAB ? (a.blob + pd.e2lab) : nullptr;
+    const int rowwords = a.n1s * ESZ / 4;
 
-    // shared: per-lane-column histogram [256][32], the P_i list, per-warp (U, B, D[cs]), adjT
+    // shared: per-lane-column histogram [256][32], the P_i list, per-warp regions, adjT, CSR
     int *s_hist = reinterpret_cast<int *>(dsmem);
     int32_t *s_pq = s_hist + 256 * 32;
     int32_t *s_pl = s_pq + a.n1r;
     uint32_t *wbase = reinterpret_cast<uint32_t *>(s_pl + a.n1r);
-    uint32_t *sU = wbase + wib * (64 + cs);
-    uint32_t *sB = sU + 32;
+    const int WWORDS = large_warp_words(cs, a.csz, a.n1s, ESZ), PFW = large_pf_words(cs, a.csz, a.n1s, ESZ);
+    const int CNTW = cs * a.csz / 4;
+    const bool brancher = wib < a.nwa;
+    uint32_t *sB = wbase + wib * WWORDS;
     int *D = reinterpret_cast<int *>(sB + 32);
+    uint32_t *pfb = sB + 32 + cs;
+    uint32_t *after = wbase + a.nwa * WWORDS;
     const uint32_t *adjT = a.adjT;
     if (a.adjT_in_smem) {
-        uint32_t *t = wbase + NWB * (64 + cs);
-        for (int x = threadIdx.x; x < W * cs; x += LNT) t[x] = __ldg(a.adjT + x);
-        adjT = t;
+        for (int x = threadIdx.x; x < W * cs; x += LNT) after[x] = __ldg(a.adjT + x);
+        adjT = after;
+        after += W * cs;
     }
-    for (int x = lane; x < cs; x += 32) D[x] = 0;
-    // root: lambda empty, nothing used, PED 0
+    const int32_t *nptr = a.nptr;
+    const uint32_t *nbr = a.nbr;
+    if (a.csr_in_smem) {
+        const int np = (n2 + 4) & ~3, nn = 2 * pd.m2;
+        int32_t *sp = reinterpret_cast<int32_t *>(after);
+        for (int x = threadIdx.x; x <= n2; x += LNT) sp[x] = __ldg(a.nptr + x);
+        for (int x = threadIdx.x; x < nn; x += LNT) after[np + x] = __ldg(a.nbr + x);
+        nptr = sp;
+        nbr = after + np;
+    }
+    if (brancher)
+        for (int x = lane; x < cs; x += 32) D[x] = 0;
+    auto adjw = [&](int j, int w) -> uint32_t { // word w of g2's bit row j
+        return a.adjT_in_smem ? adjT[w * cs + j] : __ldg(adj2 + (int64_t)j * W + w);
+    };
+    // root: lambda empty, nothing used, PED 0 -- row 0 of level -1 (buffer 1)
     if (blockIdx.x == 0) {
-        if (threadIdx.x == 0) a.ped[0][0] = 0;
-        for (int w = threadIdx.x; w < W; w += LNT) a.used[0][w] = 0u;
-        for (int u = threadIdx.x; u < cs; u += LNT) reinterpret_cast<CntT *>(a.cnt[0])[u] = 0;
+        if (threadIdx.x == 0) { a.sel_p[0] = 0; a.sel_j[0] = -1; a.sel_ped[0] = 0; }
+        for (int w = threadIdx.x; w < W; w += LNT) a.used[1][w] = 0u;
+        for (int u = threadIdx.x; u < cs; u += LNT) reinterpret_cast<CntT *>(a.cnt[1])[u] = 0;
     }
     block_sync();
     grid.sync();
 
-    int N = 1, lo = 0, hi = 0, cur = 0, ps = 0;
+    int N = 1, lo = 0, hi = 0, ps = 0;
     int64_t children = 0, parents = 0, algb = 0;
+    int64_t tph[5] = {0, 0, 0, 0, 0}, nhist = 0;
+    uint64_t tlast = 0;
+    auto tick = [&](int ph) { // phase clock (thread 0 of CTA 0, after a grid barrier)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (ph >= 0) tph[ph] += (int64_t)(t - tlast);
+            tlast = t;
+        }
+    };
+    tick(-1);
     for (int i = 0; i < n1; ++i) {
-        const int32_t *Pped = a.ped[cur];
-        const uint32_t *Pused = a.used[cur];
-        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[cur]);
-        const MapT *Pmap = reinterpret_cast<const MapT *>(a.map[cur]);
-        int32_t *Qped = a.ped[cur ^ 1];
-        uint32_t *Qused = a.used[cur ^ 1];
-        CntT *Qcnt = reinterpret_cast<CntT *>(a.cnt[cur ^ 1]);
-        MapT *Qmap = reinterpret_cast<MapT *>(a.map[cur ^ 1]);
+        const int pv = (i + 1) & 1, cu = i & 1; // buffers of level i-1 (the parents' parents) and level i
+        const uint32_t *Pused = a.used[pv];
+        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[pv]);
+        const MapT *Pmap = reinterpret_cast<const MapT *>(a.map[pv]);
+        uint32_t *Qused = a.used[cu];
+        CntT *Qcnt = reinterpret_cast<CntT *>(a.cnt[cu]);
+        MapT *Qmap = reinterpret_cast<MapT *>(a.map[cu]);
         const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
         for (int k = threadIdx.x; k < d; k += LNT) {
             s_pq[k] = __ldg(pqg + pbeg + k);
@@ -218,108 +279,182 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
         const int edd = c.edel * d, ee = c.edel + c.eins, pedDel = c.vdel + edd;
         // cB by scatter over neighbour lists, or by popcount over the nonzero words of B_p (uniform choice)
         const bool scatter = LAB || (d * a.degw * 8 < S * min(W, d) * 13);
-        const int chunk = (N + GW - 1) / GW;
+        const int chunk = (N + GW - 1) / GW; // B / C1: static contiguous code ranges per warp
         const int p0 = min(N, gw * chunk), p1 = min(N, p0 + chunk);
+        const int cchunk = (N + gridDim.x - 1) / gridDim.x; // A: this CTA's parents, taken dynamically
+        const int cb0 = min(N, (int)blockIdx.x * cchunk), cb1 = min(N, cb0 + cchunk);
+        constexpr int EPW = 4 / ESZ;                            // lambda entries per 32-bit word
+        const int wprev = i > 0 ? (i - 1 + EPW - 1) / EPW : 0; // lambda words of a level-(i-1) row (entries 0..i-2)
+        const int wcur = (i + EPW - 1) / EPW;                   // ... of a level-i row (entries 0..i-1)
         int base = lo, below = 0;
         bool first = true, keepall = false;
         int tcode = 0, rq = 0;
+        block_sync(); // P_i staged
 
         for (;;) { // ---------------- A + T ----------------
             // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
             // (each of the N parents has a deletion child <= U_i): their codes skip the histogram.
             const int capc = (N >= K) ? max(0, min(win, hi + pedDel - base + 1)) : win;
             for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
-            if (threadIdx.x == 0) s_cnt = 0;
+            if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; }
             if (blockIdx.x == 0)
                 for (int k = threadIdx.x; k < 256; k += LNT) a.hist[((ps + 1) % 3) * 256 + k] = 0;
             block_sync();
             int wcount = 0;
-            for (int p = p0; p < p1; ++p) {
-                const int pedp = Pped[p];
-                const MapT *mrow = Pmap + (int64_t)p * a.n1s;
-                int nused = 0;
-                for (int w = lane; w < W; w += 32) {
-                    const uint32_t uw = Pused[(int64_t)p * W + w];
-                    sU[w] = uw;
-                    nused += __popc(uw);
-                    if (!scatter) sB[w] = 0u;
-                }
-                nused = __reduce_add_sync(FULL, nused);
-                __syncwarp();
-                uint32_t nzb = 0;
-                if (scatter) {
-                    // D[u] += 1 (+ 1 << 16 on a label mismatch) for every neighbour u of every image t_k
-                    for (int k0 = 0; k0 < d; k0 += 32) {
-                        const int kk = k0 + lane;
-                        const int tk = kk < d ? (int)mrow[s_pq[kk]] : DELV;
-                        const int lk = (LAB && kk < d) ? s_pl[kk] : 0;
-                        const int kn = min(32, d - k0);
-                        for (int z = 0; z < kn; ++z) {
-                            const int t = __shfl_sync(FULL, tk, z);
-                            if (t == DELV) continue;
-                            const int lz = LAB ? __shfl_sync(FULL, lk, z) : 0;
-                            const int e1 = __ldg(a.nptr + t + 1);
-                            for (int e = __ldg(a.nptr + t) + lane; e < e1; e += 32) {
-                                const uint32_t v = __ldg(a.nbr + e);
-                                atomicAdd(&D[v & 0xffffu], (LAB && (int)(v >> 16) != lz) ? 0x10001 : 1);
-                            }
-                        }
+            if (brancher) {
+                // 3-stage pipeline per warp: descriptor loads (registers) -> row prefetch (cp.async into the
+                // ring) -> materialise + expand.  Buffer slot: [cnt | used | lambda | k, p, j, ped].
+                auto grab = [&]() -> int {
+                    int v = 0;
+                    if (lane == 0) v = atomicAdd(&s_next, 1);
+                    return __shfl_sync(FULL, v, 0);
+                };
+                auto load_desc = [&](int k) -> int { // lanes 0..2: p, j, ped of parent k
+                    if (k >= cb1 || lane > 2) return 0;
+                    return lane == 0 ? a.sel_p[k] : (lane == 1 ? a.sel_j[k] : a.sel_ped[k]);
+                };
+                auto issue = [&](int k, int dv, uint32_t *pf) {
+                    const int p = __shfl_sync(FULL, dv, 0);
+                    if (lane < 3) pf[PFW - 4 + 1 + lane] = (uint32_t)dv;
+                    if (lane == 0) pf[PFW - 4] = (uint32_t)k;
+                    if (k < cb1) {
+                        const uint8_t *crow8 = reinterpret_cast<const uint8_t *>(Pcnt + (int64_t)p * cs);
+                        for (int x = lane; x < CNTW / 4; x += 32) cpa16(pf + 4 * x, crow8 + 16 * x);
+                        for (int w = lane; w < W; w += 32) cpa4(pf + CNTW + w, Pused + (int64_t)p * W + w);
+                        const uint32_t *mr = reinterpret_cast<const uint32_t *>(Pmap) + (int64_t)p * rowwords;
+                        for (int w = lane; w < wprev; w += 32) cpa4(pf + CNTW + 32 + w, mr + w);
                     }
-                } else {
-                    for (int k = lane; k < d; k += 32) {
-                        const int t = mrow[s_pq[k]];
-                        if (t != DELV) atomicOr(&sB[t >> 5], 1u << (t & 31));
+                    cpa_commit(); // (possibly empty group: keeps the ring's group count uniform)
+                };
+                int kn = grab(), dn = load_desc(kn);
+                issue(kn, dn, pfb);
+                kn = grab();
+                dn = load_desc(kn);
+                for (int r = 0;; ++r) {
+                    const int kx = kn, dx = dn;
+                    kn = grab();
+                    dn = load_desc(kn);                               // descriptor of the parent after next
+                    issue(kx, dx, pfb + ((r + 1) % LPF) * PFW);       // rows of the next parent
+                    cpa_wait<1>();
+                    __syncwarp();
+                    uint32_t *pf = pfb + (r % LPF) * PFW;
+                    const int k = (int)pf[PFW - 4];
+                    if (k >= cb1) break; // (parents are taken in increasing order: the rest is empty)
+                    const int j = (int)pf[PFW - 2], pedp = (int)pf[PFW - 1];
+                    const int jn = (j >= 0 && j < n2) ? j : -1; // target used by this node's last step
+                    uint32_t *sU = pf + CNTW;
+                    uint32_t *mrow = pf + CNTW + 32;
+                    if (lane == 0) a.ped[cu][k] = pedp;
+                    // materialise row k of level i: used | j, lambda + entry i-1, counters + adj2 row j
+                    int nused = 0;
+                    for (int w = lane; w < W; w += 32) {
+                        uint32_t uw = sU[w];
+                        if (jn >= 0 && (jn >> 5) == w) uw |= 1u << (jn & 31);
+                        sU[w] = uw;
+                        Qused[(int64_t)k * W + w] = uw;
+                        nused += __popc(uw);
+                        if (!scatter) sB[w] = 0u;
+                    }
+                    nused = __reduce_add_sync(FULL, nused);
+                    if (i > 0) {
+                        const int hw = (i - 1) / EPW, sh = ((i - 1) % EPW) * 8 * ESZ;
+                        const uint32_t e = (j == n2) ? (uint32_t)DELV : (uint32_t)j;
+                        uint32_t *dst = reinterpret_cast<uint32_t *>(Qmap) + (int64_t)k * rowwords;
+                        for (int w = lane; w < wcur; w += 32) {
+                            uint32_t word = w < wprev ? mrow[w] : 0u;
+                            if (w == hw) {
+                                word = (word & ~((uint32_t)DELV << sh)) | (e << sh);
+                                mrow[w] = word;
+                            }
+                            dst[w] = word;
+                        }
                     }
                     __syncwarp();
-                    nzb = __ballot_sync(FULL, lane < W && sB[lane] != 0u);
-                }
-                __syncwarp();
-                const int pb = pedp - base + 1 + edd;
-                uint8_t *crow = a.codes + (int64_t)p * cs;
-                const CntT *cr = Pcnt + (int64_t)p * cs;
-                for (int s = 0; s < S; ++s) {
-                    const int u0 = 128 * s + 4 * lane;
-                    const typename C4::V cv = C4::load(cr, u0);
-                    const uint32_t ub = (sU[min(u0 >> 5, 31)] >> (u0 & 31)) & 0xfu;
-                    int cb[4] = {0, 0, 0, 0}, ms[4] = {0, 0, 0, 0};
+                    auto tmap = [&](int q) -> int {
+                        return (int)((mrow[(q * ESZ) >> 2] >> (8 * ((q * ESZ) & 3))) & (uint32_t)DELV);
+                    };
+                    uint32_t nzb = 0;
                     if (scatter) {
-                        int4 *dp = reinterpret_cast<int4 *>(D + u0);
-                        const int4 dv = *dp;
-                        *dp = make_int4(0, 0, 0, 0);
-                        cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
-                        if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
+                        // D[u] += 1 (+ 1 << 16 on a label mismatch) for every neighbour u of every image t_k
+                        for (int k0 = 0; k0 < d; k0 += 32) {
+                            const int kk = k0 + lane;
+                            const int tk = kk < d ? tmap(s_pq[kk]) : DELV;
+                            const int lk = (LAB && kk < d) ? s_pl[kk] : 0;
+                            const int kn2 = min(32, d - k0);
+                            for (int z = 0; z < kn2; ++z) {
+                                const int t = __shfl_sync(FULL, tk, z);
+                                if (t == DELV) continue;
+                                const int lz = LAB ? __shfl_sync(FULL, lk, z) : 0;
+                                const int e1 = nptr[t + 1];
+                                // the neighbours of one t are distinct: plain read-modify-write, no atomics
+                                for (int e = nptr[t] + lane; e < e1; e += 32) {
+                                    const uint32_t v = nbr[e];
+                                    D[v & 0xffffu] += (LAB && (int)(v >> 16) != lz) ? 0x10001 : 1;
+                                }
+                                __syncwarp();
+                            }
+                        }
                     } else {
-                        uint32_t m = nzb;
-                        while (m) {
-                            const int w = __ffs(m) - 1;
-                            m &= m - 1;
-                            const uint4 av = *reinterpret_cast<const uint4 *>(adjT + (int64_t)w * cs + u0);
-                            const uint32_t bw = sB[w];
-                            cb[0] += __popc(av.x & bw); cb[1] += __popc(av.y & bw);
-                            cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
+                        for (int q = lane; q < d; q += 32) {
+                            const int t = tmap(s_pq[q]);
+                            if (t != DELV) atomicOr(&sB[t >> 5], 1u << (t & 31));
                         }
+                        __syncwarp();
+                        nzb = __ballot_sync(FULL, lane < W && sB[lane] != 0u);
                     }
-                    uint32_t word = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int u = u0 + b;
-                        int code;
-                        if (u < n2 && !((ub >> b) & 1u)) {
-                            const int x = pb + (int)((mm >> (4 * s + b)) & 1ull) * c.vsub + c.eins * C4::get(cv, b) -
-                                          ee * cb[b] + (LAB ? c.esub * ms[b] : 0);
-                            code = min(max(x, 0), win + 1);
-                        } else if (u == n2) {
-                            code = rank_code(pedp + pedDel, base, win); // deletion child (reading C5)
+                    __syncwarp();
+                    const int pb = pedp - base + 1 + edd;
+                    uint8_t *crow = a.codes + (int64_t)k * cs;
+                    const CntT *cr = reinterpret_cast<const CntT *>(pf);
+                    CntT *qc = Qcnt + (int64_t)k * cs;
+                    for (int s = 0; s < S; ++s) {
+                        const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
+                        typename C4::V cv = C4::load(cr, u0);
+                        if (jn >= 0 && wu < W) cv = C4::add_bits(cv, (adjw(jn, wu) >> (u0 & 31)) & 0xfu);
+                        if (first) C4::store(qc, u0, cv);
+                        const uint32_t ub = (sU[min(wu, 31)] >> (u0 & 31)) & 0xfu;
+                        const uint32_t mnib = (uint32_t)(mm >> (4 * s)) & 0xfu;
+                        int cb[4] = {0, 0, 0, 0}, ms[4] = {0, 0, 0, 0};
+                        if (scatter) {
+                            int4 *dp = reinterpret_cast<int4 *>(D + u0);
+                            const int4 dv = *dp;
+                            *dp = make_int4(0, 0, 0, 0);
+                            cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
+                            if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
                         } else {
-                            code = CODE_INVALID;
+                            uint32_t m = nzb;
+                            while (m) {
+                                const int w = __ffs(m) - 1;
+                                m &= m - 1;
+                                const uint4 av = *reinterpret_cast<const uint4 *>(adjT + (int64_t)w * cs + u0);
+                                const uint32_t bw = sB[w];
+                                cb[0] += __popc(av.x & bw); cb[1] += __popc(av.y & bw);
+                                cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
+                            }
                         }
-                        if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
-                        word |= (uint32_t)code << (8 * b);
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int u = u0 + b;
+                            int code;
+                            if (u < n2 && !((ub >> b) & 1u)) {
+                                const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
+                                              (LAB ? c.esub * ms[b] : 0);
+                                code = min(max(x, 0), win + 1);
+                            } else if (u == n2) {
+                                code = rank_code(pedp + pedDel, base, win); // deletion child (reading C5)
+                            } else {
+                                code = CODE_INVALID;
+                            }
+                            if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
+                            word |= (uint32_t)code << (8 * b);
+                        }
+                        *reinterpret_cast<uint32_t *>(crow + u0) = word;
                     }
-                    *reinterpret_cast<uint32_t *>(crow + u0) = word;
+                    wcount += n2 - nused + 1;
+                    __syncwarp();
                 }
-                wcount += n2 - nused + 1;
-                __syncwarp();
+                cpa_wait<0>();
             }
             if (first && lane == 0) atomicAdd((unsigned long long *)&s_cnt, (unsigned long long)wcount);
             block_sync();
@@ -333,6 +468,7 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
             block_sync();
             grid.sync();
+            tick(0);
             // T: every CTA derives the same threshold from the global histogram
             const int64_t ci = a.ci[i];
             keepall = (ci <= K);
@@ -352,6 +488,7 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
                         const int y = __shfl_up_sync(FULL, incl, o);
                         if (lane >= o) incl += y;
                     }
+                    if (blockIdx.x == 0 && lane == 31) nhist += incl;
                     const unsigned hm = __ballot_sync(FULL, below + incl >= K);
                     if (hm) {
                         const int L = __ffs(hm) - 1;
@@ -386,21 +523,31 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
         // ---------------- B: per-warp counts of codes < t and == t ----------------
         const uint4 *cvec = reinterpret_cast<const uint4 *>(a.codes + (int64_t)p0 * cs);
         const int nvec = (p1 - p0) * cs / 16;
+        const int vpr = cs / 16; // 16-byte code vectors per parent row
         const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
         const uint32_t inv4 = (uint32_t)CODE_INVALID * 0x01010101u;
+        const uint4 inv = make_uint4(inv4, inv4, inv4, inv4);
         auto masks = [&](uint32_t v, uint32_t &mlt, uint32_t &meq) {
             if (keepall) { mlt = ~bytes_eq(v, inv4) & 0x80808080u; meq = 0u; }
             else { mlt = bytes_lt(v, t4); meq = bytes_eq(v, t4); }
         };
         {
             int lt = 0, eq = 0;
-            for (int x = lane; x < nvec; x += 32) {
-                const uint4 v = cvec[x];
-                uint32_t m0, e0;
-                masks(v.x, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                masks(v.y, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                masks(v.z, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                masks(v.w, m0, e0); lt += __popc(m0); eq += __popc(e0);
+            for (int x0 = 0; x0 < nvec; x0 += 128) { // four 16-byte loads in flight per lane
+                uint4 v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int x = x0 + 32 * t + lane;
+                    v[t] = x < nvec ? cvec[x] : inv;
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    uint32_t m0, e0;
+                    masks(v[t].x, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                    masks(v[t].y, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                    masks(v[t].z, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                    masks(v[t].w, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                }
             }
             lt = __reduce_add_sync(FULL, lt);
             eq = __reduce_add_sync(FULL, eq);
@@ -408,6 +555,7 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
         }
         block_sync();
         grid.sync();
+        tick(1);
 
         // ---------------- prefix for this CTA's warps (computed redundantly per CTA) ----------------
         {
@@ -424,51 +572,79 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
         for (int w = blockIdx.x * NWB; w < gw; ++w) { ltpre += a.wlt[w]; eqpre += a.weq[w]; }
         const int Nn = keepall ? (int)a.ci[i] : K;
 
-        // ---------------- C1: compact survivors in (parent, child) order ----------------
+        // ---------------- C1: compact survivors in (parent, child) order, with their PEDs ----------------
         {
+            int mylo = 0x7fffffff, myhi = (int)0x80000000;
             int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
-            for (int x0 = 0; x0 < nvec; x0 += 32) {
-                const int x = x0 + lane;
-                const uint4 v = x < nvec ? cvec[x] : make_uint4(inv4, inv4, inv4, inv4);
-                uint32_t ml[4], me[4];
-                masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
-                masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
-                const int nlt = __popc(ml[0]) + __popc(ml[1]) + __popc(ml[2]) + __popc(ml[3]);
-                const int neq = __popc(me[0]) + __popc(me[1]) + __popc(me[2]) + __popc(me[3]);
-                if (!__any_sync(FULL, (nlt | neq) != 0)) continue;
-                int einc = neq;
+            for (int xb = 0; xb < nvec; xb += 128) {
+                uint4 vv[4];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(FULL, einc, o);
-                    if (lane >= o) einc += y;
+                for (int t = 0; t < 4; ++t) {
+                    const int x = xb + 32 * t + lane;
+                    vv[t] = x < nvec ? cvec[x] : inv;
                 }
-                const int adm = min(neq, max(0, rq - (eq_seen + einc - neq))); // ties admitted in code order
-                const int keep = nlt + adm;
-                int kinc = keep;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(FULL, kinc, o);
-                    if (lane >= o) kinc += y;
-                }
-                int pos = out + kinc - keep, ecnt = 0;
-                if (keep) {
+                for (int t = 0; t < 4; ++t) {
+                    const int x = xb + 32 * t + lane;
+                    const uint4 v = vv[t];
+                    uint32_t ml[4], me[4];
+                    masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
+                    masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
+                    const int nlt = __popc(ml[0]) + __popc(ml[1]) + __popc(ml[2]) + __popc(ml[3]);
+                    const int neq = __popc(me[0]) + __popc(me[1]) + __popc(me[2]) + __popc(me[3]);
+                    if (!__any_sync(FULL, (nlt | neq) != 0)) continue;
+                    int einc = neq;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        uint32_t m = ml[w], e = me[w];
-                        while (e && ecnt < adm) { const uint32_t lowb = e & (0u - e); m |= lowb; e ^= lowb; ++ecnt; }
-                        while (m) {
-                            const int by = (__ffs(m) - 1) >> 3;
-                            m &= m - 1;
-                            const int64_t g = (int64_t)p0 * cs + 16 * (int64_t)x + 4 * w + by;
-                            const int p = (int)(g / cs);
-                            a.sel_p[pos] = p;
-                            a.sel_j[pos] = (int)(g - (int64_t)p * cs);
-                            ++pos;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL, einc, o);
+                        if (lane >= o) einc += y;
+                    }
+                    const int adm = min(neq, max(0, rq - (eq_seen + einc - neq))); // ties admitted in code order
+                    const int keep = nlt + adm;
+                    int kinc = keep;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULL, kinc, o);
+                        if (lane >= o) kinc += y;
+                    }
+                    if (keep) {
+                        int pos = out + kinc - keep, ecnt = 0;
+                        const int pr = x / vpr, k = p0 + pr;       // a vector never straddles two rows
+                        const int ub = 16 * (x - pr * vpr);
+                        const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            uint32_t m = ml[w], e = me[w];
+                            while (e && ecnt < adm) { const uint32_t lowb = e & (0u - e); m |= lowb; e ^= lowb; ++ecnt; }
+                            while (m) {
+                                const int by = (__ffs(m) - 1) >> 3;
+                                m &= m - 1;
+                                const int u = ub + 4 * w + by;
+                                const int code = (int)((words[w] >> (8 * by)) & 0xffu);
+                                int ped;
+                                if (code >= 1 && code <= win) ped = base + code - 1;
+                                else // saturated code: recompute from the parent's materialised row (rare)
+                                    ped = large_child_scalar<MapT, CntT, LAB>(
+                                        a, d, s_pq, s_pl, a.ped[cu][k], Qcnt + (int64_t)k * cs,
+                                        Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
+                                a.sel_p[pos] = k;
+                                a.sel_j[pos] = u;
+                                a.sel_ped[pos] = ped;
+                                mylo = min(mylo, ped);
+                                myhi = max(myhi, ped);
+                                ++pos;
+                            }
                         }
                     }
+                    out += __shfl_sync(FULL, kinc, 31);
+                    eq_seen += __shfl_sync(FULL, einc, 31);
                 }
-                out += __shfl_sync(FULL, kinc, 31);
-                eq_seen += __shfl_sync(FULL, einc, 31);
+            }
+            mylo = __reduce_min_sync(FULL, mylo);
+            myhi = __reduce_max_sync(FULL, myhi);
+            if (lane == 0 && mylo != 0x7fffffff) {
+                atomicMin(&a.lo[i + 1], mylo);
+                atomicMax(&a.hi[i + 1], myhi);
             }
         }
         if (blockIdx.x == 0 && threadIdx.x == 0 && a.levels_out) {
@@ -476,93 +652,56 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
             a.levels_out[3 * i + 1] = a.ci[i];
             a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
         }
-        block_sync();
-        grid.sync();
-
-        // ---------------- C2: next frontier, a warp per survivor row ----------------
-        {
-            int mylo = 0x7fffffff, myhi = (int)0x80000000;
-            constexpr int EPW = 4 / sizeof(MapT); // lambda entries per 32-bit word
-            const int wpr = (i + EPW) / EPW, hw = i / EPW, sh = (i % EPW) * 8 * (int)sizeof(MapT);
-            const int rowwords = a.n1s * (int)sizeof(MapT) / 4;
-            const uint32_t emask = (sizeof(MapT) == 1) ? 0xffu : 0xffffu;
-            for (int k = gw; k < Nn; k += GW) {
-                const int p = a.sel_p[k], j = a.sel_j[k];
-                const CntT *pr = Pcnt + (int64_t)p * cs;
-                if (lane == 0) {
-                    const int code = a.codes[(int64_t)p * cs + j];
-                    int ped;
-                    if (code >= 1 && code <= win) ped = base + code - 1;
-                    else // saturated code: recompute (rare)
-                        ped = large_child_scalar<MapT, CntT, LAB>(a, d, s_pq, s_pl, Pped[p], pr, Pmap + (int64_t)p * a.n1s,
-                                                                  j, adj2, e2, vl1i, vl2);
-                    Qped[k] = ped;
-                    mylo = min(mylo, ped);
-                    myhi = max(myhi, ped);
-                }
-                for (int w = lane; w < W; w += 32) {
-                    uint32_t v = Pused[(int64_t)p * W + w];
-                    if (j < n2 && (j >> 5) == w) v |= 1u << (j & 31);
-                    Qused[(int64_t)k * W + w] = v;
-                }
-                CntT *qr = Qcnt + (int64_t)k * cs;
-                for (int u0 = 4 * lane; u0 < cs; u0 += 128) {
-                    typename C4::V v = C4::load(pr, u0);
-                    if (j < n2 && (u0 >> 5) < W) v = C4::add_bits(v, (__ldg(adj2 + (int64_t)j * W + (u0 >> 5)) >> (u0 & 31)) & 0xfu);
-                    C4::store(qr, u0, v);
-                }
-                const uint32_t *src = reinterpret_cast<const uint32_t *>(Pmap) + (int64_t)p * rowwords;
-                uint32_t *dst = reinterpret_cast<uint32_t *>(Qmap) + (int64_t)k * rowwords;
-                for (int w = lane; w < wpr; w += 32) {
-                    uint32_t word = src[w];
-                    if (w == hw) {
-                        const uint32_t e = (j == n2) ? (uint32_t)DELV : (uint32_t)j;
-                        word = (word & ~(emask << sh)) | (e << sh);
-                    }
-                    dst[w] = word;
-                }
-            }
-            if (lane == 0 && mylo != 0x7fffffff) {
-                atomicMin(&a.lo[i + 1], mylo);
-                atomicMax(&a.hi[i + 1], myhi);
-            }
-        }
         parents += N;
-        algb += (int64_t)N * (4 + (int)sizeof(MapT) * d) + (int64_t)Nn * ((int)sizeof(MapT) * (2 * i + 1) + 8);
+        algb += (int64_t)N * (4 + ESZ * d) + (int64_t)Nn * (ESZ * (2 * i + 1) + 8);
         block_sync();
         grid.sync();
+        tick(2);
         N = Nn;
         lo = a.lo[i + 1];
         hi = a.hi[i + 1];
-        cur ^= 1;
     }
 
     // ---------------- finalize: completion + argmin ----------------
     {
-        const int32_t *Pped = a.ped[cur];
-        const uint32_t *Pused = a.used[cur];
-        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[cur]);
-        for (int k = gw; k < N; k += GW) { // warp per survivor
+        const int pv = (n1 + 1) & 1; // rows of level n1 - 1 (the final nodes' parents)
+        const uint32_t *Pused = a.used[pv];
+        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[pv]);
+        for (int k = gw; k < N; k += GW) { // warp per final node (p, j)
+            const int p = a.sel_p[k], j = a.sel_j[k], ped = a.sel_ped[k];
+            const int jn = (j >= 0 && j < n2) ? j : -1;
             int usedc = 0, e2u2 = 0;
-            for (int w = lane; w < W; w += 32) usedc += __popc(Pused[(int64_t)k * W + w]);
-            for (int u = lane; u < n2; u += 32)
-                if ((Pused[(int64_t)k * W + (u >> 5)] >> (u & 31)) & 1u) e2u2 += (int)Pcnt[(int64_t)k * cs + u];
+            for (int w = lane; w < W; w += 32) {
+                uint32_t uw = Pused[(int64_t)p * W + w];
+                if (jn >= 0 && (jn >> 5) == w) uw |= 1u << (jn & 31);
+                usedc += __popc(uw);
+            }
+            for (int u = lane; u < n2; u += 32) {
+                uint32_t uw = Pused[(int64_t)p * W + (u >> 5)];
+                if (jn >= 0 && (jn >> 5) == (u >> 5)) uw |= 1u << (jn & 31);
+                if ((uw >> (u & 31)) & 1u) {
+                    int cu = (int)Pcnt[(int64_t)p * cs + u];
+                    if (jn >= 0) cu += (int)((adjw(jn, u >> 5) >> (u & 31)) & 1u);
+                    e2u2 += cu;
+                }
+            }
             usedc = __reduce_add_sync(FULL, usedc);
             e2u2 = __reduce_add_sync(FULL, e2u2); // every edge among used vertices counted from both ends
             if (lane == 0) {
-                const int64_t total = (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) +
-                                      (int64_t)c.eins * (pd.m2 - e2u2 / 2);
+                const int64_t total = (int64_t)ped + (int64_t)c.vins * (n2 - usedc) + (int64_t)c.eins * (pd.m2 - e2u2 / 2);
                 atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)k);
             }
         }
         block_sync();
         grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 31) a.out[9] = nhist;
         if (blockIdx.x == 0) {
             const unsigned long long best = *a.best;
             const int kb = (int)(best & 0xffffffffull);
-            const MapT *row = reinterpret_cast<const MapT *>(a.map[cur]) + (int64_t)kb * a.n1s;
+            const int p = a.sel_p[kb], j = a.sel_j[kb];
+            const MapT *row = reinterpret_cast<const MapT *>(a.map[pv]) + (int64_t)p * a.n1s;
             for (int q = threadIdx.x; q < n1; q += LNT) {
-                const int t = row[q];
+                const int t = (q == n1 - 1) ? ((j == n2) ? DELV : j) : (int)row[q];
                 a.map_out[q] = (t == DELV) ? -1 : t;
             }
             if (threadIdx.x == 0) {
@@ -570,6 +709,8 @@ __global__ void __launch_bounds__(LNT, 2) kbest_large_kernel(const LargeArgs a) 
                 a.out[1] = children;
                 a.out[2] = parents;
                 a.out[3] = algb;
+                tick(4);
+                for (int x = 0; x < 5; ++x) a.out[4 + x] = tph[x];
             }
         }
     }

@@ -16,4 +16,4 @@ for idx in sel:
     st = h.stats()
     print(f"n={n} p={p} K={K}: cost={r['cost']} wall={1e3*(t1-t0):.1f} ms device={st['device_ms']:.1f} ms "
           f"children={r['children']:.3e} nodes/s={r['children']/(st['device_ms']/1e3):.3e} alg_bytes={st['alg_bytes']:.3e} "
-          f"GB/s={st['alg_bytes']/(st['device_ms']/1e3)/1e9:.1f}", flush=True)
+          f"GB/s={st['alg_bytes']/(st['device_ms']/1e3)/1e9:.1f} phases(A,B,C1,C2,fin)ms={[round(x, 1) for x in st['phase_ms']]} hist_frac={st['hist_children']/max(1,r['children']):.3f}", flush=True)
