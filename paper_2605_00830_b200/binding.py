@@ -75,7 +75,7 @@ def lib(path: Optional[str] = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("FASTGED_LIB") or LIB_PATH  # FASTGED_LIB: A/B builds (scripts/ab_build.py)
     if not os.path.exists(path):
         raise FastGedError(ERR_CUDA, f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
     L = C.CDLL(path)

@@ -92,6 +92,15 @@ struct BatchArgs {
     int64_t *levels_out;    // NULL, or [3 * n1] for a single-pair launch
 };
 
+#ifdef FG_PROF
+// profiling builds only: per-phase SM cycles of CTA thread 0, summed over CTAs, printed by the last CTA
+__device__ unsigned long long fg_prof_cyc[8];
+__device__ unsigned int fg_prof_done;
+#define FG_PH(k) do { if (threadIdx.x == 0) { const long long now_ = clock64(); ph_[k] += now_ - ph_last_; ph_last_ = now_; } } while (0)
+#else
+#define FG_PH(k) do { } while (0)
+#endif
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -164,7 +173,8 @@ __device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, 
 template <int W, bool LAB, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const BatchArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
-    __shared__ int s_hist[(NT / 32) * 129];
+    // per-warp rank-code histograms, row stride 132: code c at [c + 3], codes 1..128 16-byte aligned
+    __shared__ __align__(16) int s_hist[(NT / 32) * 132];
     __shared__ int s_tmp[144 + 32];
     __shared__ int s_item, s_lo;
     __shared__ uint32_t s_pnext[32]; // bit q: v_q is an earlier neighbour of v_{i+1} (n1 <= 1024)
@@ -197,11 +207,28 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     auto fbt = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + (int64_t)Kc * (4 + 4 * W)); };
     auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 8 * W); };
 
+#ifdef FG_PROF
+    long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last_ = clock64();
+#endif
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(a.work, 1);
         block_sync();
         const int item = s_item;
-        if (item >= a.ngroup) return;
+        if (item >= a.ngroup) {
+#ifdef FG_PROF
+            if (threadIdx.x == 0) {
+                for (int k = 0; k < 8; ++k) atomicAdd(&fg_prof_cyc[k], (unsigned long long)ph_[k]);
+                __threadfence();
+                if (atomicAdd(&fg_prof_done, 1u) == gridDim.x - 1) {
+                    printf("FGPROF W=%d setup %llu P %llu A+T %llu S2 %llu decode %llu U %llu final %llu S1 %llu\n", W, fg_prof_cyc[0],
+                           fg_prof_cyc[1], fg_prof_cyc[2], fg_prof_cyc[3], fg_prof_cyc[4], fg_prof_cyc[5], fg_prof_cyc[6], fg_prof_cyc[7]);
+                    for (int k = 0; k < 8; ++k) fg_prof_cyc[k] = 0;
+                    fg_prof_done = 0;
+                }
+            }
+#endif
+            return;
+        }
         const PairDesc pd = a.descs[a.order[item]];
         const int n1 = pd.n1, n2 = pd.n2, n2p = pd.n2p;
         const int32_t *vl1 = reinterpret_cast<const int32_t *>(a.blob + pd.vl1);
@@ -250,7 +277,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 s_pq[k] = __ldg(pq + pbeg + k);
                 s_pl[k] = __ldg(pl + pbeg + k);
             }
-            for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
+            for (int k = threadIdx.x; k < NW * 132; k += NT) s_hist[k] = 0;
             const int vl1i = __ldg(vl1 + i);
             uint32_t Vm[W], Mm[W]; // existing targets / label mismatches, bit u of word u >> 5
 #pragma unroll
@@ -262,6 +289,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
             block_sync(); // P_i list and zeroed histograms visible
+            FG_PH(0);
 
             // ---------------- P: parents -> used masks in shared memory, compact code offsets ----------------
             // Parent p has f_p = n2 - |used_p| substitution children + 1 deletion child; its rank codes
@@ -297,6 +325,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 for (int x = ci; x < ((ci + 3) & ~3); ++x) codes[x] = (uint8_t)CODE_INVALID;
             }
             block_sync();
+            FG_PH(1);
 
             // ---------------- A + T: branch, rank codes, histogram, threshold ----------------
             const int chunk = (N + NW - 1) / NW;
@@ -304,7 +333,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             int base = lo, below = 0, tcode = 256, rq = 0, below_add = 0;
             bool keepall = ci <= K, retry = false;
             // exact histogram of rank codes 1..win (win <= 127): one private row per warp, shared atomics
-            int *whist = s_hist + warp * 129;
+            int *whist = s_hist + warp * 132 + 3;
             auto hist_add = [&](int code) {
                 if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
             };
@@ -440,15 +469,16 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 }
                 block_sync();
                 { // T: every warp derives the same threshold from the per-warp histograms (4 codes per lane)
-                    int hv[4], sum = 0;
+                    int hv[4] = {0, 0, 0, 0}; // codes 4 lane + 1 .. 4 lane + 4 (one 16-byte read per warp row)
+                    for (int w = 0; w < NW; ++w) {
+                        const int4 h4 = *reinterpret_cast<const int4 *>(s_hist + w * 132 + 4 + 4 * lane);
+                        hv[0] += h4.x; hv[1] += h4.y; hv[2] += h4.z; hv[3] += h4.w;
+                    }
+                    int sum = 0;
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
-                        const int bb = 4 * lane + 1 + x; // codes 1..128
-                        int v = 0;
-                        if (bb <= win)
-                            for (int w = 0; w < NW; ++w) v += s_hist[w * 129 + bb];
-                        hv[x] = v;
-                        sum += v;
+                        if (4 * lane + 1 + x > win) hv[x] = 0;
+                        sum += hv[x];
                     }
                     int incl = sum;
 #pragma unroll
@@ -476,10 +506,11 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 block_sync(); // all warps have read the histograms
                 below += below_add;
                 base += win;
-                for (int k = threadIdx.x; k < NW * 129; k += NT) s_hist[k] = 0;
+                for (int k = threadIdx.x; k < NW * 132; k += NT) s_hist[k] = 0;
                 block_sync();
             }
 
+            FG_PH(2);
             // ---------------- S: selection by segment scan over the compact code words ----------------
             int Nn;
             {
@@ -506,6 +537,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 }
                 int ltpre, eqpre, lttot, eqtot;
                 block_scan2<NT>(lt, eq, ltpre, eqpre, lttot, eqtot, s_tmp);
+                FG_PH(7);
                 Nn = keepall ? lttot : K;
                 int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
                 if (lt + (eqpre < rq ? eq : 0) > 0) {
@@ -550,6 +582,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 }
             }
             block_sync();
+            FG_PH(3);
 
             // ---------------- decode survivors: (parent p, rank in p) -> (p, child j), PED from the code ----------------
             for (int k = threadIdx.x; k < Nn; k += NT) {
@@ -570,8 +603,10 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 sel[k] = ((uint32_t)p << 8) | (uint32_t)j;
             }
             block_sync();
+            FG_PH(4);
 
             // ---------------- U: write the next frontier (coalesced over k) ----------------
+            int pmin = 0x7fffffff;
             for (int k = threadIdx.x; k < Nn; k += NT) {
                 int ped = selped[k];
                 if (ped < 0) { // saturated rank code: recompute the child's PED (rare)
@@ -599,14 +634,15 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                     }
                 }
                 Qped[k] = ped;
-                atomicMin(&s_lo, ped);
-            }
-            for (int x = threadIdx.x; x < W * Nn; x += NT) {
-                const int w = x / Nn, k = x - w * Nn;
                 const uint32_t v = sel[k];
                 const int p = (int)(v >> 8), j = (int)(v & 255u);
-                QusedT[(int64_t)w * Kc + k] = sU[w * Kc + p] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+#pragma unroll
+                for (int w = 0; w < W; ++w)
+                    QusedT[(int64_t)w * Kc + k] = sU[w * Kc + p] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+                pmin = min(pmin, ped);
             }
+            pmin = __reduce_min_sync(FULL, (unsigned)pmin); // PEDs are >= 0: unsigned min = signed min
+            if (lane == 0 && pmin != 0x7fffffff) atomicMin(&s_lo, pmin);
             {
                 const int nk4 = (Nn + 3) >> 2;
                 const bool inext = (i + 1 < n1) && ((s_pnext[i >> 5] >> (i & 31)) & 1u);
@@ -666,6 +702,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             // B_alg(i) = N_i (4 + b d_i) + N_{i+1} (b i + 4) + N_{i+1} (b (i+1) + 4), b = 1
             algb += (int64_t)N * (4 + d) + (int64_t)Nn * (2 * i + 9);
             block_sync();
+            FG_PH(5);
             N = Nn;
             lo = s_lo;
             cur ^= 1;
@@ -705,6 +742,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 const int t = PmapT[(int64_t)q * Kc + kb];
                 a.map_out[pd.map_out + q] = (t == MAP_DEL) ? -1 : t;
             }
+            FG_PH(6);
             if (threadIdx.x == 0) {
                 const int pidx = a.order[item];
                 a.cost_out[pidx] = (int64_t)(best >> 32);

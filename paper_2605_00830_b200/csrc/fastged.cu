@@ -400,7 +400,10 @@ int64_t frontier_cap(int n1, int n2, int64_t k) {
     return std::min(mx, k);
 }
 
-constexpr int BATCH_NT = 256;
+#ifndef FG_BATCH_NT
+#define FG_BATCH_NT 256
+#endif
+constexpr int BATCH_NT = FG_BATCH_NT; // threads per CTA of the batched kernel (A/B: -DFG_BATCH_NT=...)
 constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batches into two pipelined chunks
 
 void *batch_kernel_for(int W, bool lab, bool smem) {
