@@ -66,7 +66,7 @@ struct PairDesc {
 // ped/u/b/t/codes/sel: byte offsets into shared memory (SMEM launches) or into the CTA's global
 // scratch after its two frontier buffers (large-K launches).
 struct SmemPlan {
-    int32_t pq, pl, e2, adj, ped, u, b, t, codes, sel, bytes;
+    int32_t pq, pl, e2, adj, adjh, ped, u, b, t, codes, sel, bytes;
 };
 
 struct BatchArgs {
@@ -134,6 +134,11 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
     return pos;
 }
 
+// Slot of a single-bit word b = 1 << bt under the de Bruijn hash (b * 0x077CB531) >> 27, a bijection of
+// 0..31: the wide branch loop addresses the g2 row of target 32 w + bt through this slot, so it needs
+// neither the bit index nor the BREV/FLO pair of __ffs (both on the quarter-rate XU pipe, like POPC).
+__host__ __device__ __forceinline__ uint32_t db_slot(uint32_t b) { return (b * 0x077CB531u) >> 27; }
+
 __device__ __forceinline__ int rank_code(int ped, int base, int win) {
     const int x = ped - base + 1;
     return x < 0 ? 0 : (x > win ? win + 1 : x);
@@ -194,6 +199,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
     uint8_t *s_e2 = dsmem + a.sm.e2;
     uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
+    uint32_t *sAdjH = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjh); // the same rows at [32 w + db_slot(bit)][W]
     int32_t *selped = reinterpret_cast<int32_t *>(wk + a.sm.ped); // PED of survivor k (-1: recompute)
     uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [W][K]
     int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
@@ -238,7 +244,12 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
         const int32_t *pl = reinterpret_cast<const int32_t *>(a.blob + pd.pl);
         const uint32_t *adj2 = reinterpret_cast<const uint32_t *>(a.blob + pd.adj2);
 
-        for (int x = threadIdx.x; x < n2 * W; x += NT) sAdj[x] = __ldg(adj2 + x);
+        for (int x = threadIdx.x; x < n2 * W; x += NT) {
+            const uint32_t v = __ldg(adj2 + x);
+            const int u = x / W, y = x - u * W;
+            sAdj[x] = v;
+            sAdjH[(32 * (u >> 5) + (int)db_slot(1u << (u & 31))) * W + y] = v;
+        }
         if (LAB) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
             uint32_t *dst = reinterpret_cast<uint32_t *>(s_e2);
@@ -354,16 +365,18 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         int r = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
-                            auto child_code = [&](int bt) -> int {
-                                const int u = 32 * w + bt;
+                            // child for the free target whose bit is lb (lowest set bit of F, no bit index)
+                            auto child_code = [&](uint32_t lb) -> int {
+                                const uint32_t *row = sAdjH + (32 * w + (int)db_slot(lb)) * W;
                                 int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
                                 for (int x = 0; x < W; ++x) {
-                                    const uint32_t rw = sAdj[u * W + x];
+                                    const uint32_t rw = row[x];
                                     cnt += __popc(rw & U[x]);
                                     if (!LAB) cb += __popc(rw & B[x]);
                                 }
                                 if (LAB) { // edge label of (u, t_k) vs the g1 edge label (v_i, v_q_k)
+                                    const int u = 32 * w + __ffs(lb) - 1;
 #pragma unroll
                                     for (int k = 0; k < DMAX; ++k) {
                                         if (tl[k] == MAP_DEL) continue;
@@ -373,17 +386,17 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                     }
                                 }
                                 // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
-                                const int x = pb + (int)((Mm[w] >> bt) & 1u) * c.vsub + c.eins * cnt - ee * cb + c.esub * mis;
+                                const int x = pb + ((Mm[w] & lb) ? c.vsub : 0) + c.eins * cnt - ee * cb + c.esub * mis;
                                 return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
                             while (F) { // two free targets per iteration (independent chains)
-                                const int b0 = __ffs(F) - 1;
-                                F &= F - 1;
+                                const uint32_t l0 = F & (0u - F);
+                                F ^= l0;
                                 const bool two = F != 0u;
-                                const int b1 = two ? __ffs(F) - 1 : b0;
-                                F &= F - 1;
-                                const int c0 = child_code(b0), c1 = child_code(b1);
+                                const uint32_t l1 = two ? (F & (0u - F)) : l0;
+                                F ^= l1 & (0u - (uint32_t)two);
+                                const int c0 = child_code(l0), c1 = child_code(l1);
                                 crow[r] = (uint8_t)c0;
                                 atomicAdd(&whist[c0], 1); // codes 0 and win+1 land in unused bins
                                 if (two) {
