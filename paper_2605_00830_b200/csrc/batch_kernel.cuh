@@ -139,6 +139,10 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
 // neither the bit index nor the BREV/FLO pair of __ffs (both on the quarter-rate XU pipe, like POPC).
 __host__ __device__ __forceinline__ uint32_t db_slot(uint32_t b) { return (b * 0x077CB531u) >> 27; }
 
+// Row stride (words) of the slot-addressed g2 rows: W adjacency words + the level's vertex cost cv(i, u),
+// padded so a row is one 8- or 16-byte shared load.
+__host__ __device__ constexpr int hrow_stride(int W) { return W + 1 <= 2 ? 2 : (W + 1 <= 4 ? 4 : 8); }
+
 __device__ __forceinline__ int rank_code(int ped, int base, int win) {
     const int x = ped - base + 1;
     return x < 0 ? 0 : (x > win ? win + 1 : x);
@@ -199,7 +203,9 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
     uint8_t *s_e2 = dsmem + a.sm.e2;
     uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
-    uint32_t *sAdjH = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjh); // the same rows at [32 w + db_slot(bit)][W]
+    // the same rows at [32 w + db_slot(bit)][HRS], word W = cv(i, u) of the current level
+    uint32_t *sAdjH = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjh);
+    constexpr int HRS = hrow_stride(W);
     int32_t *selped = reinterpret_cast<int32_t *>(wk + a.sm.ped); // PED of survivor k (-1: recompute)
     uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [W][K]
     int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             const uint32_t v = __ldg(adj2 + x);
             const int u = x / W, y = x - u * W;
             sAdj[x] = v;
-            sAdjH[(32 * (u >> 5) + (int)db_slot(1u << (u & 31))) * W + y] = v;
+            sAdjH[(32 * (u >> 5) + (int)db_slot(1u << (u & 31))) * HRS + y] = v;
         }
         if (LAB) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
@@ -297,6 +303,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 const int l2 = (u < n2) ? __ldg(vl2 + u) : 0;
                 Vm[s] = __ballot_sync(FULL, u < n2);
                 Mm[s] = __ballot_sync(FULL, u < n2 && l2 != vl1i);
+                if (u < n2) sAdjH[(32 * s + (int)db_slot(1u << lane)) * HRS + W] = (l2 != vl1i) ? (uint32_t)c.vsub : 0u;
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
             block_sync(); // P_i list and zeroed histograms visible
@@ -367,13 +374,23 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         for (int w = 0; w < W; ++w) {
                             // child for the free target whose bit is lb (lowest set bit of F, no bit index)
                             auto child_code = [&](uint32_t lb) -> int {
-                                const uint32_t *row = sAdjH + (32 * w + (int)db_slot(lb)) * W;
+                                const uint32_t *row = sAdjH + (32 * w + (int)db_slot(lb)) * HRS;
+                                uint32_t rv[HRS]; // W row words + cv(i, u), one vector load
+                                if constexpr (HRS == 2) {
+                                    const uint2 q = *reinterpret_cast<const uint2 *>(row);
+                                    rv[0] = q.x; rv[1] = q.y;
+                                } else {
+#pragma unroll
+                                    for (int h = 0; h < HRS; h += 4) {
+                                        const uint4 q = *reinterpret_cast<const uint4 *>(row + h);
+                                        rv[h] = q.x; rv[h + 1] = q.y; rv[h + 2] = q.z; rv[h + 3] = q.w;
+                                    }
+                                }
                                 int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
                                 for (int x = 0; x < W; ++x) {
-                                    const uint32_t rw = row[x];
-                                    cnt += __popc(rw & U[x]);
-                                    if (!LAB) cb += __popc(rw & B[x]);
+                                    cnt += __popc(rv[x] & U[x]);
+                                    if (!LAB) cb += __popc(rv[x] & B[x]);
                                 }
                                 if (LAB) { // edge label of (u, t_k) vs the g1 edge label (v_i, v_q_k)
                                     const int u = 32 * w + __ffs(lb) - 1;
@@ -386,24 +403,24 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                     }
                                 }
                                 // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
-                                const int x = pb + ((Mm[w] & lb) ? c.vsub : 0) + c.eins * cnt - ee * cb + c.esub * mis;
+                                const int x = pb + (int)rv[W] + c.eins * cnt - ee * cb + c.esub * mis;
                                 return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
-                            while (F) { // two free targets per iteration (independent chains)
-                                const uint32_t l0 = F & (0u - F);
-                                F ^= l0;
-                                const bool two = F != 0u;
-                                const uint32_t l1 = two ? (F & (0u - F)) : l0;
-                                F ^= l1 & (0u - (uint32_t)two);
-                                const int c0 = child_code(l0), c1 = child_code(l1);
-                                crow[r] = (uint8_t)c0;
-                                atomicAdd(&whist[c0], 1); // codes 0 and win+1 land in unused bins
-                                if (two) {
-                                    crow[r + 1] = (uint8_t)c1;
-                                    atomicAdd(&whist[c1], 1);
-                                }
-                                r += two ? 2 : 1;
+                            while (F) { // four free targets per iteration (independent chains); lb = 0: no child
+                                uint32_t lz[4];
+#pragma unroll
+                                for (int z = 0; z < 4; ++z) { lz[z] = F & (0u - F); F ^= lz[z]; }
+                                int cz[4];
+#pragma unroll
+                                for (int z = 0; z < 4; ++z) cz[z] = child_code(lz[z]);
+#pragma unroll
+                                for (int z = 0; z < 4; ++z)
+                                    if (z == 0 || lz[z]) {
+                                        crow[r + z] = (uint8_t)cz[z];
+                                        atomicAdd(&whist[cz[z]], 1); // codes 0 and win+1 land in unused bins
+                                    }
+                                r += 1 + (lz[1] != 0u) + (lz[2] != 0u) + (lz[3] != 0u);
                             }
                         }
                         const int cdel = rank_code(pedp + dDel, base, win); // deletion child (C5)

@@ -499,7 +499,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.sm.pl = (int)sm; sm += align16(4 * (size_t)a.n1max);
         a.sm.e2 = (int)sm; sm += key.lab ? align16((size_t)n2p * n2p) : 0;
         a.sm.adj = (int)sm; sm += align16(4 * (size_t)std::max(n2max, 1) * W);
-        a.sm.adjh = (int)sm; sm += align16(4 * (size_t)32 * W * W);
+        a.sm.adjh = (int)sm; sm += align16(4 * (size_t)32 * W * fg::hrow_stride(W));
         // per-level work arrays
         size_t wk = 0;
         auto put = [&](int32_t &field, size_t bytes) { field = (int)wk; wk += align16(bytes); };
