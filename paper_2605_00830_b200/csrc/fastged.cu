@@ -726,6 +726,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     occ = 1; // one CTA per SM (the grid barrier cost grows with the CTA count)
     const int grid = occ * h->sms;
     const int GW = grid * (fg::LNT / 32);
+    if (grid > fg::LMAXGRID) fail(FASTGED_ERR_ARG, "large-mode grid %d exceeds %d CTAs", grid, fg::LMAXGRID);
     // device buffers
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
@@ -739,6 +740,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
     size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(80);
     size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
+    size_t o_ctl = take(4 * (size_t)grid), o_cte = take(4 * (size_t)grid), o_rowc = take(4 * (size_t)Kc);
     CK(h->lbuf.reserve(off));
     uint8_t *B = (uint8_t *)h->lbuf.p;
     CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
@@ -777,6 +779,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.lo = (int32_t *)(B + o_lo);
     a.hi = (int32_t *)(B + o_hi);
     a.wlt = (int32_t *)(B + o_wlt); a.weq = (int32_t *)(B + o_weq);
+    a.ctl = (int32_t *)(B + o_ctl); a.cte = (int32_t *)(B + o_cte); a.rowc = (int32_t *)(B + o_rowc);
     a.best = (unsigned long long *)(B + o_best);
     a.out = (int64_t *)(B + o_out);
     a.map_out = (int32_t *)(B + o_mapout);

@@ -47,6 +47,7 @@ namespace cg = cooperative_groups;
 
 constexpr int LNT = 512; // threads per CTA of the large kernel (one CTA per SM)
 constexpr int LPF = 2;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
+constexpr int LMAXGRID = 256; // CTAs of the large kernel (one per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cpa4(void *sdst, const void *gsrc) {
@@ -125,7 +126,9 @@ struct LargeArgs {
     int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
     int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
-    int32_t *wlt, *weq;     // [total warps]
+    int32_t *wlt, *weq;     // [total warps] codes < t / == t in the warp's B range
+    int32_t *ctl, *cte;     // [grid] the same per CTA
+    int32_t *rowc;          // [Kc] per parent row: (codes < t) | (codes == t) << 16
     unsigned long long *best;
     int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes,
                             // [4..8] ns in phases A+T, B, C1, -, finalize (CTA 0's clock),
@@ -180,6 +183,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     constexpr int ESZ = (int)sizeof(MapT);
     __shared__ int s_pre[2];
     __shared__ int s_red[2][NWB];
+    __shared__ int s_cpre[2][LMAXGRID]; // exclusive prefix of the per-CTA counts
     __shared__ long long s_cnt;
     __shared__ int s_next; // A: next parent of this CTA's range (warps take parents dynamically)
     cg::grid_group grid = cg::this_grid();
@@ -520,9 +524,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             base += win; // the K-th smallest PED lies beyond the window: slide it (codes 0 = kept)
         }
 
-        // ---------------- B: per-warp counts of codes < t and == t ----------------
-        const uint4 *cvec = reinterpret_cast<const uint4 *>(a.codes + (int64_t)p0 * cs);
-        const int nvec = (p1 - p0) * cs / 16;
+        // ---------------- B: per-row counts of codes < t and == t (warp per row, static ranges) ----------------
         const int vpr = cs / 16; // 16-byte code vectors per parent row
         const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
         const uint32_t inv4 = (uint32_t)CODE_INVALID * 0x01010101u;
@@ -531,62 +533,88 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             if (keepall) { mlt = ~bytes_eq(v, inv4) & 0x80808080u; meq = 0u; }
             else { mlt = bytes_lt(v, t4); meq = bytes_eq(v, t4); }
         };
+        auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(a.codes + (int64_t)k * cs)[x]; };
         {
-            int lt = 0, eq = 0;
-            for (int x0 = 0; x0 < nvec; x0 += 128) { // four 16-byte loads in flight per lane
-                uint4 v[4];
+            int wl = 0, we = 0;
+            for (int k0 = p0; k0 < p1; k0 += 4) { // four rows per step: their loads are in flight together
+                int lt[4] = {0, 0, 0, 0}, eq[4] = {0, 0, 0, 0};
+                for (int x = lane; x < vpr; x += 32) {
+                    uint4 v[4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int x = x0 + 32 * t + lane;
-                    v[t] = x < nvec ? cvec[x] : inv;
+                    for (int r = 0; r < 4; ++r) v[r] = (k0 + r < p1) ? rowvec(k0 + r, x) : inv;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        uint32_t m0, e0;
+                        masks(v[r].x, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        masks(v[r].y, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        masks(v[r].z, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        masks(v[r].w, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                    }
                 }
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    uint32_t m0, e0;
-                    masks(v[t].x, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                    masks(v[t].y, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                    masks(v[t].z, m0, e0); lt += __popc(m0); eq += __popc(e0);
-                    masks(v[t].w, m0, e0); lt += __popc(m0); eq += __popc(e0);
+                for (int r = 0; r < 4; ++r) {
+                    const int l = __reduce_add_sync(FULL, lt[r]), e = __reduce_add_sync(FULL, eq[r]);
+                    if (lane == 0 && k0 + r < p1) a.rowc[k0 + r] = l | (e << 16);
+                    wl += l;
+                    we += e;
                 }
             }
-            lt = __reduce_add_sync(FULL, lt);
-            eq = __reduce_add_sync(FULL, eq);
-            if (lane == 0) { a.wlt[gw] = lt; a.weq[gw] = eq; }
+            if (lane == 0) { a.wlt[gw] = wl; a.weq[gw] = we; s_red[0][wib] = wl; s_red[1][wib] = we; }
+            block_sync();
+            if (threadIdx.x == 0) {
+                int cl = 0, ce = 0;
+                for (int w = 0; w < NWB; ++w) { cl += s_red[0][w]; ce += s_red[1][w]; }
+                a.ctl[blockIdx.x] = cl;
+                a.cte[blockIdx.x] = ce;
+            }
         }
         block_sync();
         grid.sync();
         tick(1);
 
-        // ---------------- prefix for this CTA's warps (computed redundantly per CTA) ----------------
-        {
-            int slt = 0, seq = 0;
-            const int first_w = blockIdx.x * NWB;
-            for (int g = threadIdx.x; g < first_w; g += LNT) { slt += a.wlt[g]; seq += a.weq[g]; }
-            slt = __reduce_add_sync(FULL, slt);
-            seq = __reduce_add_sync(FULL, seq);
-            if (lane == 0) { s_red[0][wib] = slt; s_red[1][wib] = seq; }
-            block_sync();
+        // ---------------- prefix of the per-CTA counts (every CTA, redundantly) ----------------
+        if (wib == 0) {
+            int cl = 0, ce = 0, rl = 0, re = 0;
+            for (int g0 = 0; g0 < (int)gridDim.x; g0 += 32) {
+                const int g = g0 + lane;
+                const int l = g < (int)gridDim.x ? a.ctl[g] : 0, e = g < (int)gridDim.x ? a.cte[g] : 0;
+                int il = l, ie = e;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int yl = __shfl_up_sync(FULL, il, o), ye = __shfl_up_sync(FULL, ie, o);
+                    if (lane >= o) { il += yl; ie += ye; }
+                }
+                if (g < (int)gridDim.x) { s_cpre[0][g] = rl + il - l; s_cpre[1][g] = re + ie - e; }
+                rl += __shfl_sync(FULL, il, 31);
+                re += __shfl_sync(FULL, ie, 31);
+            }
+            (void)cl; (void)ce;
         }
-        int ltpre = 0, eqpre = 0;
-        for (int w = 0; w < NWB; ++w) { ltpre += s_red[0][w]; eqpre += s_red[1][w]; }
-        for (int w = blockIdx.x * NWB; w < gw; ++w) { ltpre += a.wlt[w]; eqpre += a.weq[w]; }
+        block_sync();
         const int Nn = keepall ? (int)a.ci[i] : K;
 
         // ---------------- C1: compact survivors in (parent, child) order, with their PEDs ----------------
+        // Rows are dealt round-robin over all warps (survivors cluster in the rows of a few good parents,
+        // so the static B ranges would leave a handful of warps with all of them); rows without a survivor
+        // are skipped without reading their codes.  A row's output offset = prefix of the CTAs before its
+        // B owner + the owner CTA's warps before the owner warp + the owner's rows before it.
         {
             int mylo = 0x7fffffff, myhi = (int)0x80000000;
-            int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
-            for (int xb = 0; xb < nvec; xb += 128) {
-                uint4 vv[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int x = xb + 32 * t + lane;
-                    vv[t] = x < nvec ? cvec[x] : inv;
-                }
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int x = xb + 32 * t + lane;
-                    const uint4 v = vv[t];
+            for (int k = gw; k < N; k += GW) {
+                const int rc = a.rowc[k];
+                if (!keepall && (rc & 0xffff) == 0 && (rc >> 16) <= 0) continue; // (no code < t, no tie)
+                if (keepall && rc == 0) continue;
+                const int ow = k / chunk, oc = ow / NWB;
+                int pl = 0, pe = 0;
+                for (int w = oc * NWB + lane; w < ow; w += 32) { pl += a.wlt[w]; pe += a.weq[w]; }
+                for (int r = ow * chunk + lane; r < k; r += 32) { const int v = a.rowc[r]; pl += v & 0xffff; pe += v >> 16; }
+                const int ltpre = s_cpre[0][oc] + __reduce_add_sync(FULL, pl);
+                const int eqpre = s_cpre[1][oc] + __reduce_add_sync(FULL, pe);
+                if (!keepall && (rc & 0xffff) == 0 && eqpre >= rq) continue; // its ties are all past the quota
+                int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
+                for (int xb = 0; xb < vpr; xb += 32) {
+                    const int x = xb + lane;
+                    const uint4 v = x < vpr ? rowvec(k, x) : inv;
                     uint32_t ml[4], me[4];
                     masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
                     masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
@@ -609,8 +637,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                     if (keep) {
                         int pos = out + kinc - keep, ecnt = 0;
-                        const int pr = x / vpr, k = p0 + pr;       // a vector never straddles two rows
-                        const int ub = 16 * (x - pr * vpr);
+                        const int ub = 16 * x;
                         const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                         for (int w = 0; w < 4; ++w) {
