@@ -333,10 +333,12 @@ def run_pair(args, rank, local_rank, world):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    dev_ms, wall = 0.0, time.perf_counter()
+    dev_ms, kern_ms, wall = 0.0, 0.0, time.perf_counter()
     for _ in range(args.steps):
         r2 = h.solve_pair(g1, g2, w.costs, K)
-        dev_ms += h.stats()["device_ms"]
+        st2 = h.stats()
+        dev_ms += st2["device_ms"]
+        kern_ms += st2["branch_ms"]  # CUDA events around the cooperative kernel, on its stream
         assert r2["cost"] == r["cost"]
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - wall
@@ -347,6 +349,26 @@ def run_pair(args, rank, local_rank, world):
     dev_ms, wall = (float(x) for x in vals.tolist())
     st = h.stats()
     h.close()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("large_kernel_dram_bytes_per_launch")
+    except Exception:
+        pass
+    kern_s = kern_ms / args.steps / 1e3
+    ach = st["alg_bytes"] / kern_s / 1e9 if (world == 1 and kern_s > 0) else None
+    roof = {"bound": "hbm", "kernel": "kbest_large_kernel (all levels of the pair in one cooperative launch)",
+            "achieved": ach, "peak": hbm_peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback",
+            "unit": "GB/s", "frac": (ach / hbm_peak) if ach else None, "traffic": traffic,
+            "alg_bytes_per_launch": st["alg_bytes"],
+            "note": "algorithmic bytes = SURVEY §8(d) D.4 per level (parent PED + lambda rows read, child rows written); "
+                    "traffic = ncu dram read+write of the same launch (counters, used masks and rank codes on top)"}
     return {
         "metric": METRIC, "value": args.steps / (dev_ms / 1e3), "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -357,6 +379,7 @@ def run_pair(args, rank, local_rank, world):
                    "cost": r["cost"]},
         "e2e": {"value": args.steps / wall, "unit": "pairs/s", "h2d_bytes_per_step": st["h2d_bytes"],
                 "d2h_bytes_per_step": st["d2h_bytes"]},
+        "roofline": roof,
         "gpu_launches": st["kernel_launches"] * args.steps,
         "clocks": clk,
     }

@@ -126,9 +126,10 @@ struct LargeArgs {
     int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
     int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
-    int32_t *wlt, *weq;     // [total warps] codes < t / == t in the warp's B range
+    int32_t *wlt, *weq;     // [total warps] codes < t / == t in the CTA's B ranges before this warp's
     int32_t *ctl, *cte;     // [grid] the same per CTA
     int32_t *rowc;          // [Kc] per parent row: (codes < t) | (codes == t) << 16
+    int32_t *rowpl, *rowpe; // [Kc] codes < t / == t in the rows of the same B range before this row
     unsigned long long *best;
     int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes,
                             // [4..8] ns in phases A+T, B, C1, -, finalize (CTA 0's clock),
@@ -536,14 +537,17 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(a.codes + (int64_t)k * cs)[x]; };
         {
             int wl = 0, we = 0;
-            for (int k0 = p0; k0 < p1; k0 += 4) { // four rows per step: their loads are in flight together
-                int lt[4] = {0, 0, 0, 0}, eq[4] = {0, 0, 0, 0};
+            constexpr int BR = 8;
+            for (int k0 = p0; k0 < p1; k0 += BR) { // BR rows per step: their loads are in flight together
+                int lt[BR], eq[BR];
+#pragma unroll
+                for (int r = 0; r < BR; ++r) { lt[r] = 0; eq[r] = 0; }
                 for (int x = lane; x < vpr; x += 32) {
-                    uint4 v[4];
+                    uint4 v[BR];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) v[r] = (k0 + r < p1) ? rowvec(k0 + r, x) : inv;
+                    for (int r = 0; r < BR; ++r) v[r] = (k0 + r < p1) ? rowvec(k0 + r, x) : inv;
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
+                    for (int r = 0; r < BR; ++r) {
                         uint32_t m0, e0;
                         masks(v[r].x, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
                         masks(v[r].y, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
@@ -552,20 +556,25 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
+                for (int r = 0; r < BR; ++r) {
                     const int l = __reduce_add_sync(FULL, lt[r]), e = __reduce_add_sync(FULL, eq[r]);
-                    if (lane == 0 && k0 + r < p1) a.rowc[k0 + r] = l | (e << 16);
+                    if (lane == 0 && k0 + r < p1) {
+                        a.rowc[k0 + r] = l | (e << 16);
+                        a.rowpl[k0 + r] = wl;
+                        a.rowpe[k0 + r] = we;
+                    }
                     wl += l;
                     we += e;
                 }
             }
-            if (lane == 0) { a.wlt[gw] = wl; a.weq[gw] = we; s_red[0][wib] = wl; s_red[1][wib] = we; }
+            if (lane == 0) { s_red[0][wib] = wl; s_red[1][wib] = we; }
             block_sync();
-            if (threadIdx.x == 0) {
+            if (lane == 0) { // this warp's prefix inside the CTA
                 int cl = 0, ce = 0;
-                for (int w = 0; w < NWB; ++w) { cl += s_red[0][w]; ce += s_red[1][w]; }
-                a.ctl[blockIdx.x] = cl;
-                a.cte[blockIdx.x] = ce;
+                for (int w = 0; w < wib; ++w) { cl += s_red[0][w]; ce += s_red[1][w]; }
+                a.wlt[gw] = cl;
+                a.weq[gw] = ce;
+                if (wib == NWB - 1) { a.ctl[blockIdx.x] = cl + wl; a.cte[blockIdx.x] = ce + we; }
             }
         }
         block_sync();
@@ -600,21 +609,37 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         // B owner + the owner CTA's warps before the owner warp + the owner's rows before it.
         {
             int mylo = 0x7fffffff, myhi = (int)0x80000000;
-            for (int k = gw; k < N; k += GW) {
-                const int rc = a.rowc[k];
-                if (!keepall && (rc & 0xffff) == 0 && (rc >> 16) <= 0) continue; // (no code < t, no tie)
-                if (keepall && rc == 0) continue;
-                const int ow = k / chunk, oc = ow / NWB;
-                int pl = 0, pe = 0;
-                for (int w = oc * NWB + lane; w < ow; w += 32) { pl += a.wlt[w]; pe += a.weq[w]; }
-                for (int r = ow * chunk + lane; r < k; r += 32) { const int v = a.rowc[r]; pl += v & 0xffff; pe += v >> 16; }
-                const int ltpre = s_cpre[0][oc] + __reduce_add_sync(FULL, pl);
-                const int eqpre = s_cpre[1][oc] + __reduce_add_sync(FULL, pe);
-                if (!keepall && (rc & 0xffff) == 0 && eqpre >= rq) continue; // its ties are all past the quota
+            // 32 rows per batch (row kb + l GW for lane l): their counts and prefixes are loaded in parallel,
+            // then the rows holding survivors are expanded one after the other, the next one's first code
+            // vector already in flight (the loop is otherwise a chain of dependent global round trips)
+            for (int kb = gw; kb < N; kb += 32 * GW) {
+                const int kl = kb + lane * GW;
+                int rc = 0, lp = 0, ep = 0;
+                bool has = false;
+                if (kl < N) {
+                    rc = a.rowc[kl];
+                    has = keepall ? rc != 0 : ((rc & 0xffff) != 0 || (rc >> 16) > 0);
+                    if (has) {
+                        const int ow = kl / chunk, oc = ow / NWB;
+                        lp = s_cpre[0][oc] + a.wlt[ow] + a.rowpl[kl];
+                        ep = s_cpre[1][oc] + a.weq[ow] + a.rowpe[kl];
+                        if (!keepall && (rc & 0xffff) == 0 && ep >= rq) has = false; // its ties are all past the quota
+                    }
+                }
+                unsigned hm = __ballot_sync(FULL, has);
+                int zn = hm ? __ffs(hm) - 1 : 0;
+                uint4 vn = (hm && lane < vpr) ? rowvec(kb + zn * GW, lane) : inv;
+                while (hm) {
+                const int z = zn;
+                hm &= hm - 1;
+                const int k = kb + z * GW;
+                const uint4 v0 = vn;
+                if (hm) { zn = __ffs(hm) - 1; vn = lane < vpr ? rowvec(kb + zn * GW, lane) : inv; }
+                const int ltpre = __shfl_sync(FULL, lp, z), eqpre = __shfl_sync(FULL, ep, z);
                 int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
                 for (int xb = 0; xb < vpr; xb += 32) {
                     const int x = xb + lane;
-                    const uint4 v = x < vpr ? rowvec(k, x) : inv;
+                    const uint4 v = xb == 0 ? v0 : (x < vpr ? rowvec(k, x) : inv);
                     uint32_t ml[4], me[4];
                     masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
                     masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
@@ -665,6 +690,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                     out += __shfl_sync(FULL, kinc, 31);
                     eq_seen += __shfl_sync(FULL, einc, 31);
+                }
                 }
             }
             mylo = __reduce_min_sync(FULL, mylo);

@@ -25,7 +25,7 @@ recs = [{w: row[idx[w]] for w in want if w in idx} for row in r[2:]]
 for x in recs:
     x["units"] = {w: units[idx[w]] for w in want if w in idx}
 json.dump(recs, open(f"profiles/{R}_ncu_full_batch.json", "w"), indent=1)
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 dram = []
 for x in recs:
     try:
@@ -37,6 +37,13 @@ valid = [d for d in dram if d is not None]
 summary = {"source": "ncu --set full --clock-control none -k regex:kbest_batch -c 3 python scripts/prof_batch.py 10000 1000 1 (the bench workload)",
            "kernels": [x['Kernel Name'] for x in recs], "dram_bytes_per_launch": dram,
            "bench_kernel_dram_bytes_per_launch": (sum(valid) / len(valid)) if valid else None}
+if os.path.exists("gpurun_out/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500 p=0.05 K=1e5)
+    o2 = subprocess.run(["ncu", "-i", "gpurun_out/prof_large5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r2 = list(csv.reader(o2.splitlines())); h2 = r2[0]; u2 = r2[1]
+    def val(k):
+        i = h2.index(k); return float(r2[2][i].replace(",", "")) * scale.get(u2[i], 1)
+    summary["large_kernel_dram_bytes_per_launch"] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+    summary["large_source"] = "ncu --set full --clock-control none -k regex:kbest_large -c 1 python scripts/prof_large.py 5"
 json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
 subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep '(int)2' 30 > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
 for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "time_large.txt", "nvsmi.txt"):
