@@ -741,7 +741,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(80);
     size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
     size_t o_ctl = take(4 * (size_t)grid), o_cte = take(4 * (size_t)grid), o_rowc = take(4 * (size_t)Kc);
-    size_t o_rowpl = take(4 * (size_t)Kc), o_rowpe = take(4 * (size_t)Kc);
+    size_t o_rowpl = take(4 * (size_t)Kc), o_rowpe = take(4 * (size_t)Kc), o_rowmin = take(4 * (size_t)Kc);
     CK(h->lbuf.reserve(off));
     uint8_t *B = (uint8_t *)h->lbuf.p;
     CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
@@ -781,7 +781,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.hi = (int32_t *)(B + o_hi);
     a.wlt = (int32_t *)(B + o_wlt); a.weq = (int32_t *)(B + o_weq);
     a.ctl = (int32_t *)(B + o_ctl); a.cte = (int32_t *)(B + o_cte); a.rowc = (int32_t *)(B + o_rowc);
-    a.rowpl = (int32_t *)(B + o_rowpl); a.rowpe = (int32_t *)(B + o_rowpe);
+    a.rowpl = (int32_t *)(B + o_rowpl); a.rowpe = (int32_t *)(B + o_rowpe); a.rowmin = (int32_t *)(B + o_rowmin);
     a.best = (unsigned long long *)(B + o_best);
     a.out = (int64_t *)(B + o_out);
     a.map_out = (int32_t *)(B + o_mapout);

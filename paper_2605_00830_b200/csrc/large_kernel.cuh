@@ -130,6 +130,7 @@ struct LargeArgs {
     int32_t *ctl, *cte;     // [grid] the same per CTA
     int32_t *rowc;          // [Kc] per parent row: (codes < t) | (codes == t) << 16
     int32_t *rowpl, *rowpe; // [Kc] codes < t / == t in the rows of the same B range before this row
+    int32_t *rowmin;        // [Kc] smallest rank code of the row (A): B reads only rows that can hold survivors
     unsigned long long *best;
     int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes,
                             // [4..8] ns in phases A+T, B, C1, -, finalize (CTA 0's clock),
@@ -412,6 +413,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     uint8_t *crow = a.codes + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
                     CntT *qc = Qcnt + (int64_t)k * cs;
+                    uint32_t rmin = 255u;
                     for (int s = 0; s < S; ++s) {
                         const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
                         typename C4::V cv = C4::load(cr, u0);
@@ -453,9 +455,12 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             }
                             if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
                             word |= (uint32_t)code << (8 * b);
+                            rmin = min(rmin, (uint32_t)code);
                         }
                         *reinterpret_cast<uint32_t *>(crow + u0) = word;
                     }
+                    rmin = __reduce_min_sync(FULL, rmin);
+                    if (lane == 0) a.rowmin[k] = (int)rmin;
                     wcount += n2 - nused + 1;
                     __syncwarp();
                 }
@@ -537,35 +542,56 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(a.codes + (int64_t)k * cs)[x]; };
         {
             int wl = 0, we = 0;
+            // 32 rows per step, one per lane; only rows whose smallest code can be selected are read
+            // (up to 8 of them with their loads in flight together)
             constexpr int BR = 8;
-            for (int k0 = p0; k0 < p1; k0 += BR) { // BR rows per step: their loads are in flight together
-                int lt[BR], eq[BR];
-#pragma unroll
-                for (int r = 0; r < BR; ++r) { lt[r] = 0; eq[r] = 0; }
-                for (int x = lane; x < vpr; x += 32) {
-                    uint4 v[BR];
-#pragma unroll
-                    for (int r = 0; r < BR; ++r) v[r] = (k0 + r < p1) ? rowvec(k0 + r, x) : inv;
+            for (int k0 = p0; k0 < p1; k0 += 32) {
+                const int kl = k0 + lane;
+                const bool q = kl < p1 && (keepall || a.rowmin[kl] <= tcode);
+                unsigned qm = __ballot_sync(FULL, q);
+                int myl = 0, mye = 0; // counts of row kl
+                while (qm) {
+                    int zr[BR];
 #pragma unroll
                     for (int r = 0; r < BR; ++r) {
-                        uint32_t m0, e0;
-                        masks(v[r].x, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                        masks(v[r].y, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                        masks(v[r].z, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                        masks(v[r].w, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        zr[r] = qm ? __ffs(qm) - 1 : -1;
+                        if (qm) qm &= qm - 1;
                     }
-                }
+                    int lt[BR], eq[BR];
 #pragma unroll
-                for (int r = 0; r < BR; ++r) {
-                    const int l = __reduce_add_sync(FULL, lt[r]), e = __reduce_add_sync(FULL, eq[r]);
-                    if (lane == 0 && k0 + r < p1) {
-                        a.rowc[k0 + r] = l | (e << 16);
-                        a.rowpl[k0 + r] = wl;
-                        a.rowpe[k0 + r] = we;
+                    for (int r = 0; r < BR; ++r) { lt[r] = 0; eq[r] = 0; }
+                    for (int x = lane; x < vpr; x += 32) {
+                        uint4 v[BR];
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) v[r] = zr[r] >= 0 ? rowvec(k0 + zr[r], x) : inv;
+#pragma unroll
+                        for (int r = 0; r < BR; ++r) {
+                            uint32_t m0, e0;
+                            masks(v[r].x, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                            masks(v[r].y, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                            masks(v[r].z, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                            masks(v[r].w, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        }
                     }
-                    wl += l;
-                    we += e;
+#pragma unroll
+                    for (int r = 0; r < BR; ++r) {
+                        const int l = __reduce_add_sync(FULL, lt[r]), e = __reduce_add_sync(FULL, eq[r]);
+                        if (lane == zr[r]) { myl = l; mye = e; }
+                    }
                 }
+                int il = myl, ie = mye;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int yl = __shfl_up_sync(FULL, il, o), ye = __shfl_up_sync(FULL, ie, o);
+                    if (lane >= o) { il += yl; ie += ye; }
+                }
+                if (kl < p1) {
+                    a.rowc[kl] = myl | (mye << 16);
+                    a.rowpl[kl] = wl + il - myl;
+                    a.rowpe[kl] = we + ie - mye;
+                }
+                wl += __shfl_sync(FULL, il, 31);
+                we += __shfl_sync(FULL, ie, 31);
             }
             if (lane == 0) { s_red[0][wib] = wl; s_red[1][wib] = we; }
             block_sync();
