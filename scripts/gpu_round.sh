@@ -13,4 +13,4 @@ timeout 600 python bench.py --workload cfg2 --steps 5 --warmup 3 --cpu-seconds 1
 timeout 600 python scripts/time_large.py > gpurun_out/time_large.txt 2>&1; echo time_large rc=$?; cat gpurun_out/time_large.txt | cut -c1-200
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu-launch rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:kbest_batch -c 3 -o gpurun_out/prof_bench python scripts/prof_batch.py 10000 1000 1 > gpurun_out/ncu_full.log 2>&1; echo ncu-full rc=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:kbest_large -c 1 -o gpurun_out/prof_large python scripts/prof_large.py 4 > gpurun_out/ncu_large.log 2>&1; echo ncu-large rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:kbest_large -c 1 -o gpurun_out/prof_large5 python scripts/prof_large.py 5 > gpurun_out/ncu_large.log 2>&1; echo ncu-large rc=$?
