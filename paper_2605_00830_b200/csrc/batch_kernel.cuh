@@ -66,7 +66,7 @@ struct PairDesc {
 // ped/u/b/t/codes/sel: byte offsets into shared memory (SMEM launches) or into the CTA's global
 // scratch after its two frontier buffers (large-K launches).
 struct SmemPlan {
-    int32_t pq, pl, e2, adj, adjh, ped, u, b, t, codes, sel, bytes;
+    int32_t pq, pl, e2, adj, adjh, ped, u, b, t, codes, sel, pidx, bytes;
 };
 
 struct BatchArgs {
@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     uint8_t *sT = wk + a.sm.t;
     uint8_t *codes = wk + a.sm.codes;
     uint32_t *sel = reinterpret_cast<uint32_t *>(wk + a.sm.sel);
+    // coarse code position -> parent index: pidx[g] = the parent owning code position 16 g
+    uint16_t *sPidx = reinterpret_cast<uint16_t *>(wk + a.sm.pidx);
 
     auto fped = [&](int b) { return reinterpret_cast<int32_t *>(scr + b * fb); };
     auto fused = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + 4 * (int64_t)Kc); };
@@ -336,7 +338,10 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             block_scan2<NT>(nloc, 0, obase, dummy, ci, dummy2, s_tmp); // ci = candidates of the level
             for (int p = pb; p < pe; ++p) {
                 sOff[p] = obase;
-                obase += row_bytes(p);
+                const int nb = row_bytes(p);
+                if (Kc <= 65535)
+                    for (int g = (obase + 15) >> 4; 16 * g < obase + nb; ++g) sPidx[g] = (uint16_t)p;
+                obase += nb;
             }
             if (threadIdx.x == 0) {
                 sOff[N] = ci;
@@ -571,13 +576,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 Nn = keepall ? lttot : K;
                 int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
                 if (lt + (eqpre < rq ? eq : 0) > 0) {
-                    // parent cursor: the last p with off_p <= 4 w0 (then advanced monotonically)
-                    int pc = 0, phi = N - 1;
-                    while (pc < phi) {
-                        const int mid = (pc + phi + 1) >> 1;
-                        if (sOff[mid] <= 4 * w0) pc = mid; else phi = mid - 1;
-                    }
-                    int off0 = sOff[pc], off1 = sOff[pc + 1];
+                    // survivors are written as flat code positions; the parent is found in the balanced decode
                     for (int x = w0; x < w1; ++x) {
                         const uint32_t v = cw[x];
                         uint32_t m;
@@ -595,10 +594,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             }
                         }
                         while (m) {
-                            const int idx = 4 * x + ((__ffs(m) - 1) >> 3);
+                            sel[out++] = (uint32_t)(4 * x + ((__ffs(m) - 1) >> 3));
                             m &= m - 1;
-                            while (off1 <= idx) { off0 = off1; off1 = sOff[++pc + 1]; }
-                            sel[out++] = ((uint32_t)pc << 8) | (uint32_t)(idx - off0); // (parent, rank in parent)
                         }
                     }
                 }
@@ -616,10 +613,21 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
 
             // ---------------- decode survivors: (parent p, rank in p) -> (p, child j), PED from the code ----------------
             for (int k = threadIdx.x; k < Nn; k += NT) {
-                const uint32_t v = sel[k];
-                const int p = (int)(v >> 8), rnk = (int)(v & 255u);
-                const int off = sOff[p];
-                const int code = codes[off + rnk];
+                const int idx = (int)sel[k];
+                int p;
+                if (Kc <= 65535) { // owner of position 16 (idx / 16), advanced to the owner of idx
+                    p = sPidx[idx >> 4];
+                    while (sOff[p + 1] <= idx) ++p;
+                } else { // last parent with off_p <= idx
+                    p = 0;
+                    int phi = N - 1;
+                    while (p < phi) {
+                        const int mid = (p + phi + 1) >> 1;
+                        if (sOff[mid] <= idx) p = mid; else phi = mid - 1;
+                    }
+                }
+                const int rnk = idx - sOff[p];
+                const int code = codes[idx];
                 selped[k] = (code >= 1 && code <= win) ? base + code - 1 : -1;
                 int j = n2; // past every target: the deletion child
                 int rr = rnk;

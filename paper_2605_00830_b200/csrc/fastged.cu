@@ -509,10 +509,11 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         put(a.sm.t, key.lab ? (size_t)fg::DMAX * Kc : 0);
         put(a.sm.codes, Kc * a.csmax);
         put(a.sm.sel, 4 * Kc);
+        put(a.sm.pidx, 2 * (Kc * a.csmax / 16 + 2));
         const bool in_smem = sm + wk + 8192 <= h->smem_optin;
         size_t smem = sm;
         if (in_smem) {
-            for (int32_t *f : {&a.sm.ped, &a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel}) *f += (int)sm;
+            for (int32_t *f : {&a.sm.ped, &a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel, &a.sm.pidx}) *f += (int)sm;
             smem += wk;
         }
         a.sm.bytes = (int)smem;
