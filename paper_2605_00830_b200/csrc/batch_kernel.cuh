@@ -561,13 +561,16 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 auto ge = [](uint32_t x, uint32_t tt) { return (((x | 0x80808080u) - tt) | x) & 0x80808080u; };
                 auto valid = [](uint32_t x) { const uint32_t y = ~x; return (((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y) & 0x80808080u; };
                 int lt = 0, eq = 0;
+                unsigned long long cmask = 0ull; // words of the run holding a code <= t (runs of <= 64 words)
                 for (int x = w0; x < w1; ++x) {
                     const uint32_t v = cw[x];
                     if (keepall) lt += __popc(valid(v));
                     else {
                         const int g0 = __popc(ge(v, t4));
+                        const int g1 = __popc(ge(v, t41));
                         lt += 4 - g0;
-                        eq += g0 - __popc(ge(v, t41));
+                        eq += g0 - g1;
+                        if (g1 != 4) cmask |= 1ull << ((x - w0) & 63);
                     }
                 }
                 int ltpre, eqpre, lttot, eqtot;
@@ -576,8 +579,15 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 Nn = keepall ? lttot : K;
                 int out = ltpre + min(rq, eqpre), eq_seen = eqpre;
                 if (lt + (eqpre < rq ? eq : 0) > 0) {
-                    // survivors are written as flat code positions; the parent is found in the balanced decode
+                    // survivors are written as flat code positions; the parent is found in the balanced decode.
+                    // Runs of <= 64 words revisit only the words pass 1 marked.
+                    const bool sparse = !keepall && seg <= 64;
                     for (int x = w0; x < w1; ++x) {
+                        if (sparse) {
+                            if (!cmask) break;
+                            x = w0 + __ffsll((long long)cmask) - 1;
+                            cmask &= cmask - 1;
+                        }
                         const uint32_t v = cw[x];
                         uint32_t m;
                         if (keepall) m = valid(v);
