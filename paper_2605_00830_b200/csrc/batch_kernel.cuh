@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     // the same rows at [32 w + db_slot(bit)][HRS], word W = cv(i, u) of the current level
     uint32_t *sAdjH = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjh);
     constexpr int HRS = hrow_stride(W);
-    int32_t *selped = reinterpret_cast<int32_t *>(wk + a.sm.ped); // PED of survivor k (-1: recompute)
     uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [W][K]
     int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
     uint8_t *sT = wk + a.sm.t;
@@ -621,7 +620,10 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             block_sync();
             FG_PH(3);
 
-            // ---------------- decode survivors: (parent p, rank in p) -> (p, child j), PED from the code ----------------
+            // ---------------- decode survivors + U part 1 (balanced: thread per survivor) ----------------
+            // flat code position -> (p, child j); PED from the code (recomputed for a saturated code);
+            // the survivor's PED and used mask go straight to the next frontier (coalesced over k)
+            int pmin = 0x7fffffff;
             for (int k = threadIdx.x; k < Nn; k += NT) {
                 const int idx = (int)sel[k];
                 int p;
@@ -638,34 +640,27 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 }
                 const int rnk = idx - sOff[p];
                 const int code = codes[idx];
-                selped[k] = (code >= 1 && code <= win) ? base + code - 1 : -1;
+                uint32_t Up[W];
                 int j = n2; // past every target: the deletion child
                 int rr = rnk;
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
-                    const uint32_t F = Vm[w] & ~sU[w * Kc + p];
+                    Up[w] = sU[w * Kc + p];
+                    const uint32_t F = Vm[w] & ~Up[w];
                     const int cnt = __popc(F);
                     if (rr >= 0 && rr < cnt) j = 32 * w + select_bit(F, rr);
                     rr -= cnt;
                 }
                 sel[k] = ((uint32_t)p << 8) | (uint32_t)j;
-            }
-            block_sync();
-            FG_PH(4);
-
-            // ---------------- U: write the next frontier (coalesced over k) ----------------
-            int pmin = 0x7fffffff;
-            for (int k = threadIdx.x; k < Nn; k += NT) {
-                int ped = selped[k];
-                if (ped < 0) { // saturated rank code: recompute the child's PED (rare)
-                    const uint32_t v = sel[k];
-                    const int p = (int)(v >> 8), j = (int)(v & 255u);
+                int ped;
+                if (code >= 1 && code <= win) ped = base + code - 1;
+                else { // saturated rank code: recompute the child's PED (rare)
                     const int pedp = Pped[p];
                     if (j == n2) ped = pedp + dDel;
                     else {
                         int cnt = 0, cb = 0, mis = 0;
 #pragma unroll
-                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & sU[w * Kc + p]);
+                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & Up[w]);
                         if (!LAB) {
 #pragma unroll
                             for (int w = 0; w < W; ++w) cb += __popc(sAdj[j * W + w] & PBT[(int64_t)w * Kc + p]);
@@ -682,15 +677,17 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                     }
                 }
                 Qped[k] = ped;
-                const uint32_t v = sel[k];
-                const int p = (int)(v >> 8), j = (int)(v & 255u);
 #pragma unroll
                 for (int w = 0; w < W; ++w)
-                    QusedT[(int64_t)w * Kc + k] = sU[w * Kc + p] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+                    QusedT[(int64_t)w * Kc + k] = Up[w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
                 pmin = min(pmin, ped);
             }
             pmin = __reduce_min_sync(FULL, (unsigned)pmin); // PEDs are >= 0: unsigned min = signed min
             if (lane == 0 && pmin != 0x7fffffff) atomicMin(&s_lo, pmin);
+            block_sync(); // the (p, j) of every survivor is in sel
+            FG_PH(4);
+
+            // ---------------- U part 2: lambda columns (and B of the next level), coalesced over k ----------------
             {
                 const int nk4 = (Nn + 3) >> 2;
                 const bool inext = (i + 1 < n1) && ((s_pnext[i >> 5] >> (i & 31)) & 1u);

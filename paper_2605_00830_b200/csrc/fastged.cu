@@ -503,7 +503,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         // per-level work arrays
         size_t wk = 0;
         auto put = [&](int32_t &field, size_t bytes) { field = (int)wk; wk += align16(bytes); };
-        put(a.sm.ped, 4 * Kc);             // survivor PEDs
+        a.sm.ped = 0;                      // (unused: survivor PEDs go straight to the next frontier)
         put(a.sm.u, 4 * Kc * W);           // parent used masks
         put(a.sm.b, 4 * (Kc + 1));         // compact code offsets
         put(a.sm.t, key.lab ? (size_t)fg::DMAX * Kc : 0);
@@ -513,7 +513,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         const bool in_smem = sm + wk + 8192 <= h->smem_optin;
         size_t smem = sm;
         if (in_smem) {
-            for (int32_t *f : {&a.sm.ped, &a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel, &a.sm.pidx}) *f += (int)sm;
+            for (int32_t *f : {&a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel, &a.sm.pidx}) *f += (int)sm;
             smem += wk;
         }
         a.sm.bytes = (int)smem;
