@@ -138,7 +138,8 @@ struct fastged_handle {
     int evused = 0;
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     DevBuf lblob, lbuf; // large single-pair mode
-    fastged_batch *tmp = nullptr, *tmp2 = nullptr; // reused by solve_batch (two pipelined chunks) / solve_pair
+    fastged_batch *tmp = nullptr;        // reused by solve_batch (first chunk) / solve_pair
+    std::vector<fastged_batch *> tmpv;  // reused by solve_batch (later pipelined chunks)
     ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1, NCCL transport)
 };
 
@@ -899,7 +900,8 @@ void fastged_destroy(fastged_handle_t *h) {
     h->lblob.release();
     h->lbuf.release();
     free_batch(h->tmp);
-    free_batch(h->tmp2);
+    for (fastged_batch *b : h->tmpv) free_batch(b);
+    h->tmpv.clear();
     h->scratch.release();
     h->levels.release();
     h->stage.release();
@@ -980,27 +982,49 @@ int fastged_solve_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph
         validate_costs(c);
         if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
         if (!h->tmp) h->tmp = new fastged_batch();
-        // Two pipelined chunks: the GPU starts on a small first chunk while the host validates and
-        // packs the rest (same stream, so the second chunk's copies and kernels queue behind it).
-        // Pairs are independent, so the chunking does not change any result.
-        const int32_t n0 = npairs >= PIPELINE_MIN_PAIRS ? std::max<int32_t>(npairs / 8, 512) : npairs;
-        fastged_batch *b0 = build_batch(h, n0, g1s, g2s, h->tmp);
-        run_batch(h, b0, c, k, nullptr, true);
-        fastged_batch *b1 = nullptr;
-        if (n0 < npairs) {
-            if (!h->tmp2) h->tmp2 = new fastged_batch();
-            b1 = build_batch(h, npairs - n0, g1s + n0, g2s + n0, h->tmp2, n0);
-            run_batch(h, b1, c, k, nullptr, false);
+        // Pipelined chunks of doubling size: the GPU starts on a small first chunk while the host
+        // validates and packs the next one (host packing is about twice as fast as the search, so the
+        // GPU is not starved after the first chunk).  Same stream: every chunk's copies and kernels
+        // queue behind the previous one's.  Pairs are independent: chunking changes no result.
+        std::vector<std::pair<int32_t, int32_t>> cuts; // (first pair, count)
+        {
+            int32_t start = 0, sz = npairs >= PIPELINE_MIN_PAIRS ? std::max<int32_t>(npairs / 16, 512) : npairs;
+            while (start < npairs) {
+                int32_t n = std::min<int32_t>(sz, npairs - start);
+                if (npairs - start - n < sz / 2) n = npairs - start; // no small tail chunk
+                cuts.push_back({start, n});
+                start += n;
+                sz *= 2;
+            }
+            if (cuts.empty()) cuts.push_back({0, 0});
         }
-        check_outputs(b0, costs_out, mappings_out);
-        download_enqueue(h, b0);
-        if (b1) download_enqueue(h, b1);
+        std::vector<fastged_batch *> bs;
+        for (size_t ci = 0; ci < cuts.size(); ++ci) {
+            fastged_batch *reuse;
+            if (ci == 0) reuse = h->tmp;
+            else {
+                while (h->tmpv.size() < ci) h->tmpv.push_back(new fastged_batch());
+                reuse = h->tmpv[ci - 1];
+            }
+            fastged_batch *b = build_batch(h, cuts[ci].second, g1s + cuts[ci].first, g2s + cuts[ci].first, reuse,
+                                           cuts[ci].first);
+            run_batch(h, b, c, k, nullptr, ci == 0);
+            bs.push_back(b);
+        }
+        int64_t map_total = 0;
+        for (fastged_batch *b : bs) map_total += b->total_map;
+        if (npairs > 0 && !costs_out) fail(FASTGED_ERR_ARG, "costs_out is NULL");
+        if (map_total > 0 && !mappings_out) fail(FASTGED_ERR_ARG, "mappings_out is NULL");
+        for (fastged_batch *b : bs) download_enqueue(h, b);
         CK(cudaStreamSynchronize(h->stream));
         finish_timing(h);
-        download_collect(h, b0, costs_out, mappings_out, children_out);
-        if (b1)
-            download_collect(h, b1, costs_out + n0, mappings_out ? mappings_out + b0->total_map : nullptr,
-                             children_out ? children_out + n0 : nullptr);
+        int64_t moff = 0;
+        for (size_t ci = 0; ci < bs.size(); ++ci) {
+            const int32_t st0 = cuts[ci].first;
+            download_collect(h, bs[ci], costs_out ? costs_out + st0 : nullptr, mappings_out ? mappings_out + moff : nullptr,
+                             children_out ? children_out + st0 : nullptr);
+            moff += bs[ci]->total_map;
+        }
         return FASTGED_OK;
     } catch (const FgError &e) {
         cudaStreamSynchronize(h->stream);

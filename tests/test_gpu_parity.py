@@ -264,7 +264,8 @@ def test_device_resident_split_matches_solve_batch(fg, handle):
 
 
 def test_pipelined_solve_batch(fg, handle):
-    """solve_batch splits >= 4096 pairs into two pipelined chunks: same results as one resident batch,
+    """solve_batch splits >= 4096 pairs into pipelined chunks of doubling size (512, 1024, 2048, 1416
+    here): same results as one resident batch,
     and a bad pair in the second chunk is reported with its global index."""
     w = synth.config_workload(2, npairs=5000)
     packed = fg.PackedGraphs(w.graphs)
