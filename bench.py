@@ -248,7 +248,8 @@ def run_ours(args, rank, local_rank, world):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get("bench_kernel_dram_bytes_per_launch")
+        if args.workload == "cfg3":  # the ncu capture is of the cfg3 bench workload
+            traffic = prof.get("bench_kernel_dram_bytes_per_launch")
     except Exception:
         pass
     line = {

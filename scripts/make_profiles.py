@@ -46,7 +46,7 @@ if os.path.exists("gpurun_out/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500
     summary["large_source"] = "ncu --set full --clock-control none -k regex:kbest_large -c 1 python scripts/prof_large.py 5"
 json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
 subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep '(int)2' 30 > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
-for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "time_large.txt", "nvsmi.txt"):
+for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "bench_ref.json", "time_large.txt", "nvsmi.txt"):
     if os.path.exists(f"gpurun_out/{f}"):
         shutil.copy(f"gpurun_out/{f}", f"profiles/{R}_{f}")
 print(open(f"profiles/{R}_launches_bench.txt").read()); print(json.dumps(summary, indent=1))
