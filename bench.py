@@ -242,7 +242,9 @@ def run_ours(args, rank, local_rank, world):
     clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     # integer lane-op peak: 4 SMSPs x (16 ALU-pipe + 16 FMA-pipe lanes) per clock per SM
     alu_peak = sms * 128 * clk_mhz * 1e6 / 1e9  # Gop/s
-    kern_s = branch_ms / args.steps / 1e3
+    # the word-width groups' launches overlap (fork/join): the kernel time of a step is the union of
+    # their intervals, i.e. the step's device time (CUDA events on the launching stream around the run)
+    kern_s = min(branch_ms, dev_ms_max) / args.steps / 1e3
     achieved = (alg_ops / args.steps) / kern_s / 1e9 if branch_ms > 0 else None
     hbm_ach = (alg_bytes / args.steps) / kern_s / 1e9 if branch_ms > 0 else None
     traffic = None

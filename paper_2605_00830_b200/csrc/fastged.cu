@@ -141,6 +141,10 @@ struct fastged_handle {
     fastged_batch *tmp = nullptr;        // reused by solve_batch (first chunk) / solve_pair
     std::vector<fastged_batch *> tmpv;  // reused by solve_batch (later pipelined chunks)
     ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1, NCCL transport)
+    // batched launches of the word-width groups run concurrently (fork/join on side streams), so the
+    // tail of one group's persistent launch overlaps the next group's start
+    std::vector<cudaStream_t> gstreams;
+    std::vector<cudaEvent_t> gevents; // [0] fork, [1..] joins
 };
 
 namespace {
@@ -468,6 +472,8 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
     }
     CK(cudaMemsetAsync(b->dwork.p, 0, 64 * sizeof(int), h->stream));
     int gi = 0;
+    struct GroupLaunch { fg::BatchArgs a; void *kern; int grid; size_t smem, per_cta; int64_t cost; };
+    std::vector<GroupLaunch> plans;
     for (auto &sp : spans) {
         const GroupKey key = sp.first;
         const size_t start = sp.second.first, cnt = sp.second.second;
@@ -527,18 +533,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BATCH_NT, smem));
         occ = std::max(occ, 1);
         int grid = (int)std::min<int64_t>((int64_t)cnt, (int64_t)occ * h->sms);
-        // bound scratch to the device: shrink the grid, never K
-        size_t need = per_cta * (size_t)grid;
-        if (need > h->scratch.cap) {
-            size_t free_b = 0, total_b = 0;
-            CK(cudaMemGetInfo(&free_b, &total_b));
-            size_t avail = free_b + h->scratch.cap;
-            if (per_cta > avail / 2) fail(FASTGED_ERR_CAPACITY, "frontier scratch %zu B per CTA exceeds device memory", per_cta);
-            while (grid > 1 && per_cta * (size_t)grid > avail * 3 / 4) grid--;
-            h->scratch.release();
-            CK(h->scratch.reserve(per_cta * (size_t)grid));
-        }
-        a.scratch = (uint8_t *)h->scratch.p;
+        a.scratch = nullptr; // set below: this group's slice of the handle's scratch
         a.scratch_stride = (int64_t)per_cta;
         a.cost_out = (int64_t *)b->dcost.p;
         a.map_out = (int32_t *)b->dmap.p;
@@ -546,17 +541,70 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.parents_out = (int64_t *)b->dpar.p;
         a.algbytes_out = (int64_t *)b->dalg.p;
         a.levels_out = levels_dev;
+        const fg::PairDesc &d0 = b->descs[order_all[start]]; // (the group's largest pair: sorted above)
+        plans.push_back(GroupLaunch{a, kern, grid, smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
+        gi++;
+    }
+    // longest pairs first across the groups too: the group holding the largest pair is launched first
+    std::stable_sort(plans.begin(), plans.end(), [](const GroupLaunch &x, const GroupLaunch &y) { return x.cost > y.cost; });
+    // scratch: one slice per group (the groups run concurrently); shrink grids, never K
+    {
+        size_t need = 0;
+        for (auto &g : plans) need += g.per_cta * (size_t)g.grid;
+        if (need > h->scratch.cap) {
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            const size_t avail = free_b + h->scratch.cap;
+            for (auto &g : plans)
+                if (g.per_cta > avail / 2) fail(FASTGED_ERR_CAPACITY, "frontier scratch %zu B per CTA exceeds device memory", g.per_cta);
+            while (need > avail * 3 / 4) { // shrink the largest grid
+                GroupLaunch *m = nullptr;
+                for (auto &g : plans) if (g.grid > 1 && (!m || g.per_cta * g.grid > m->per_cta * m->grid)) m = &g;
+                if (!m) break;
+                m->grid--;
+                need -= m->per_cta;
+            }
+            CK(cudaStreamSynchronize(h->stream)); // the previous slices may still be in use
+            for (cudaStream_t gs : h->gstreams) CK(cudaStreamSynchronize(gs));
+            h->scratch.release();
+            CK(h->scratch.reserve(need));
+        }
+        size_t off = 0;
+        for (auto &g : plans) {
+            g.a.scratch = (uint8_t *)h->scratch.p + off;
+            off += g.per_cta * (size_t)g.grid;
+        }
+    }
+    // fork: group 0 on the handle's stream, the others on side streams; join back before ev_end
+    const size_t ng = plans.size();
+    while (h->gstreams.size() + 1 < ng) {
+        cudaStream_t gs;
+        CK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+        h->gstreams.push_back(gs);
+    }
+    while (h->gevents.size() < ng + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->gevents.push_back(e);
+    }
+    if (ng > 1) CK(cudaEventRecord(h->gevents[0], h->stream));
+    for (size_t g = 0; g < ng; ++g) {
+        cudaStream_t st = g == 0 ? h->stream : h->gstreams[g - 1];
+        if (g > 0) CK(cudaStreamWaitEvent(st, h->gevents[0], 0));
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (h->flags & FASTGED_FLAG_TIMING) {
             e0 = next_event(h);
             e1 = next_event(h);
-            CK(cudaEventRecord(e0, h->stream));
+            CK(cudaEventRecord(e0, st));
         }
-        void *params[] = {(void *)&a};
-        CK(cudaLaunchKernel(kern, dim3(grid), dim3(BATCH_NT), params, smem, h->stream));
-        if (e1) CK(cudaEventRecord(e1, h->stream));
+        void *params[] = {(void *)&plans[g].a};
+        CK(cudaLaunchKernel(plans[g].kern, dim3(plans[g].grid), dim3(BATCH_NT), params, plans[g].smem, st));
+        if (e1) CK(cudaEventRecord(e1, st));
         h->stats.kernel_launches++;
-        gi++;
+        if (g > 0) {
+            CK(cudaEventRecord(h->gevents[g], st));
+            CK(cudaStreamWaitEvent(h->stream, h->gevents[g], 0));
+        }
     }
     CK(cudaEventRecord(h->ev_end, h->stream));
     b->ran = true;
@@ -909,6 +957,8 @@ void fastged_destroy(fastged_handle_t *h) {
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
     if (h->ev_end) cudaEventDestroy(h->ev_end);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    for (cudaStream_t gs : h->gstreams) cudaStreamDestroy(gs);
+    for (cudaEvent_t e : h->gevents) cudaEventDestroy(e);
     delete h;
 }
 
