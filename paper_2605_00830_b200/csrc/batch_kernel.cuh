@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     __shared__ __align__(16) int s_hist[(NT / 32) * 132];
     __shared__ int s_tmp[144 + 32];
     __shared__ int s_item, s_lo;
-    __shared__ uint32_t s_pnext[32]; // bit q: v_q is an earlier neighbour of v_{i+1} (n1 <= 1024)
+    // bit q: v_q is an earlier neighbour of v_{i+1} (n1 <= 1024); double-buffered by level parity so
+    // the buffer of level i is zeroed during level i - 1 (no barrier between zeroing and filling)
+    __shared__ uint32_t s_pnext2[2][32];
     __shared__ unsigned long long s_best;
     constexpr int NW = NT / 32;
 
@@ -270,6 +272,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
         }
         int N = 1, lo = 0, cur = 0;
         int64_t children = 0, parents = 0, algb = 0;
+        for (int x = threadIdx.x; x < 64; x += NT) (&s_pnext2[0][0])[x] = 0u;
+        block_sync(); // (previous pair's last reads of s_pnext2 / the scratch rows are done)
 
         for (int i = 0; i < n1; ++i) {
             const int32_t *Pped = fped(cur);
@@ -282,8 +286,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             uint32_t *QBT = fbt(cur ^ 1);
             const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
             // membership of P_{i+1} over q (for the next level's B, built during the update)
-            for (int x = threadIdx.x; x < 32; x += NT) s_pnext[x] = 0u;
-            block_sync();
+            uint32_t *s_pnext = s_pnext2[i & 1];
+            for (int x = threadIdx.x; x < 32; x += NT) s_pnext2[(i + 1) & 1][x] = 0u; // used last in level i - 1
             if (i + 1 < n1) {
                 const int nb = __ldg(pptr + i + 1), ne = __ldg(pptr + i + 2);
                 for (int k = nb + threadIdx.x; k < ne; k += NT) {
@@ -307,7 +311,9 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 if (u < n2) sAdjH[(32 * s + (int)db_slot(1u << lane)) * HRS + W] = (l2 != vl1i) ? (uint32_t)c.vsub : 0u;
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
-            block_sync(); // P_i list and zeroed histograms visible
+            // P_i list, zeroed histograms, P_{i+1} membership and cv words: visible to A through the
+            // barriers of P's block scan (labelled pairs read P_i in P itself)
+            if (LAB) block_sync();
             FG_PH(0);
 
             // ---------------- P: parents -> used masks in shared memory, compact code offsets ----------------
