@@ -148,7 +148,9 @@ __device__ __forceinline__ int rank_code(int ped, int base, int win) {
     return x < 0 ? 0 : (x > win ? win + 1 : x);
 }
 
-// Block-wide exclusive scan of two ints (NT threads).  Returns totals.
+// Block-wide exclusive scan of two ints (NT threads).  Returns totals.  One barrier: every warp
+// publishes its total and then reads all NT/32 of them.  s_tmp must not be rewritten before every
+// warp has read it: consecutive calls are separated by other block barriers in the kernel.
 template <int NT>
 __device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, int &atot, int &btot, int *s_tmp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -160,23 +162,18 @@ __device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, 
     }
     if (lane == 31) { s_tmp[warp] = ia; s_tmp[32 + warp] = ib; }
     block_sync();
-    if (warp == 0) {
-        int wa = lane < NT / 32 ? s_tmp[lane] : 0, wb = lane < NT / 32 ? s_tmp[32 + lane] : 0;
-        int sa = wa, sb = wb;
+    int wa = 0, wb = 0, ta = 0, tb = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int xa = __shfl_up_sync(FULL, sa, o), xb = __shfl_up_sync(FULL, sb, o);
-            if (lane >= o) { sa += xa; sb += xb; }
-        }
-        s_tmp[64 + lane] = sa - wa;
-        s_tmp[96 + lane] = sb - wb;
-        if (lane == 31) { s_tmp[128] = sa; s_tmp[129] = sb; }
+    for (int w = 0; w < NT / 32; ++w) {
+        const int x = s_tmp[w], y = s_tmp[32 + w];
+        if (w < warp) { wa += x; wb += y; }
+        ta += x;
+        tb += y;
     }
-    block_sync();
-    apre = s_tmp[64 + warp] + ia - a;
-    bpre = s_tmp[96 + warp] + ib - b;
-    atot = s_tmp[128];
-    btot = s_tmp[129];
+    apre = wa + ia - a;
+    bpre = wb + ib - b;
+    atot = ta;
+    btot = tb;
 }
 
 template <int W, bool LAB, int NT, bool SMEM>
