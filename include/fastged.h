@@ -85,7 +85,10 @@ typedef struct {
 
 /* Handle configuration.
  *   device     : CUDA ordinal
- *   stream     : cudaStream_t to launch on, or NULL = the handle creates and owns one
+ *   stream     : cudaStream_t to launch on, or NULL = the handle creates and owns one.  Batched
+ *                runs fork onto up to three side streams the handle owns (one per word-width group,
+ *                running concurrently) and join back onto this stream before a call returns or a
+ *                fastged_batch_run's work is complete on it: callers only ever order against `stream`.
  *   world_size : 1 = single GPU.  > 1 = sharded single-pair mode (every rank calls
  *                fastged_solve_pair collectively with identical inputs)
  *   rank       : 0 <= rank < world_size
