@@ -208,6 +208,8 @@ def run_ours(args, rank, local_rank, world):
     # ---- end-to-end through the public API with host buffers (H2D + search + D2H each step)
     e2e_t = []
     h2d = d2h = 0
+    # one untimed call: the handle allocates its per-chunk pinned staging on first use
+    h.solve_batch(packed, w.pair_a, w.pair_b, w.costs, w.K)
     for s in range(max(1, args.steps)):
         flush.fill_(s)
         torch.cuda.synchronize(dev)
