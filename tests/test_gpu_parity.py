@@ -81,6 +81,27 @@ def test_config2_aids_like(fg, handle, oracle):
     assert_batch_parity(fg, handle, oracle, pairs, w.costs, w.K, "cfg2")
 
 
+def test_mixed_groups_one_batch(fg, handle, oracle):
+    """One batch holding every kernel variant at once — unlabelled ER pairs of word widths 1..4 and
+    labelled molecule pairs — so the word-width/label groups run concurrently on their own streams
+    and scratch slices; also repeated through the pipelined (>= 4096 pairs) path."""
+    w3 = synth.config_workload(3, npairs=50, K=200)
+    w2 = synth.config_workload(2, npairs=50)
+    big = [synth.large_pair(n, 0.1, seed=n)[0:2] for n in (100, 120)]  # n2 in (96, 128]: W = 4
+    pairs = [w3.pair(k) for k in range(w3.npairs)] + [w2.pair(k) for k in range(w2.npairs)] + big
+    order = np.random.default_rng(7).permutation(len(pairs))
+    pairs = [pairs[k] for k in order]
+    assert_batch_parity(fg, handle, oracle, pairs, w3.costs, 200, "mixed")
+    st = handle.stats()
+    assert st["kernel_launches"] >= 5
+    many = pairs * (4100 // len(pairs) + 1)
+    gc, gm, gch = gpu_batch(fg, handle, many, w3.costs, 200)
+    base, bm, bch = gpu_batch(fg, handle, pairs, w3.costs, 200)
+    for k in range(len(many)):
+        r = k % len(pairs)
+        assert gc[k] == base[r] and np.array_equal(gm[k], bm[r]) and gch[k] == bch[r], k
+
+
 def test_config3_er_grid_sampled(fg, handle, oracle):
     """configs[2]: ER n=30..70, p=.1-.5, K=1000 — 100 pairs covering all 25 (n, p) cells, run in the
     same batched launch configuration bench.py times."""
