@@ -27,6 +27,8 @@
  * canonical frontier order (C12); survivors form the next frontier in ascending
  * (p, j) order (C13); at the last level the K survivors (selected by PED, C10)
  * get the completion cost and the argmin by (total, position) is returned.
+ * Selection is Hoare's FIND (quickselect) on the unique keys, then a sort of only the K
+ * survivors by (p, j) -- the same set a full sort would give (P5 pin).
  *
  * Parity pins: see tests/test_oracle_pins.py (worked examples S:64-76,
  * S:191-213, closed forms, brute force over all partial injections).
@@ -128,6 +130,30 @@ static int cmp_pos(const void *x, const void *y) { /* (p, j) ascending (C13) */
     const cand *a = (const cand *)x, *b = (const cand *)y;
     if (a->p != b->p) return a->p < b->p ? -1 : 1;
     return (a->j > b->j) - (a->j < b->j);
+}
+
+/* "List <- best K nodes of list_tmp" without a full sort: Hoare's FIND
+ * (quickselect).  Rearranges a[0..n) so that a[0..k) holds the k smallest keys under
+ * (PED, p, j) (C12), in no particular order.  Keys are unique, so the set is unique (SURVEY
+ * §8(c) O.3 P5) and does not depend on the pivots, which come from a fixed xorshift sequence. */
+static void select_k(cand *a, int64_t n, int64_t k) {
+    int64_t lo = 0, hi = n - 1; /* invariant: the k-th smallest lies in a[lo..hi] */
+    uint64_t rnd = 0x9E3779B97F4A7C15ull;
+    if (k <= 0 || k >= n) return;
+    while (lo < hi) {
+        rnd ^= rnd << 13; rnd ^= rnd >> 7; rnd ^= rnd << 17;
+        cand pivot = a[lo + (int64_t)(rnd % (uint64_t)(hi - lo + 1))];
+        int64_t i = lo, j = hi;
+        while (i <= j) { /* Hoare partition around the pivot key */
+            while (cmp_key(&a[i], &pivot) < 0) i++;
+            while (cmp_key(&a[j], &pivot) > 0) j--;
+            if (i <= j) { cand t = a[i]; a[i] = a[j]; a[j] = t; i++; j--; }
+        }
+        /* now a[lo..j] <= pivot <= a[i..hi], and j < i */
+        if (k - 1 <= j) hi = j;
+        else if (k - 1 >= i) lo = i;
+        else return; /* a[j+1..i-1] equal the pivot: position k-1 is settled */
+    }
 }
 
 /* Completion (C6): insert every unused g2 vertex (vins each) and
@@ -246,13 +272,18 @@ int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t 
         parents += N;
 
         /* List <- best K nodes of list_tmp: the min(K, cnt) smallest keys (C12). */
-        qsort(pool, (size_t)cnt, sizeof(cand), cmp_key);
         int64_t keep = cnt < K ? cnt : K;
+        select_k(pool, cnt, keep);
         if (levels_out) {
+            int64_t mn = -1, mx = -1;
+            for (int64_t s = 0; s < cnt; s++)
+                if (mn < 0 || pool[s].ped < mn) mn = pool[s].ped;
+            for (int64_t s = 0; s < keep; s++)
+                if (pool[s].ped > mx) mx = pool[s].ped;
             levels_out[i].frontier = N;
             levels_out[i].candidates = cnt;
-            levels_out[i].threshold = (cnt > K) ? pool[keep - 1].ped : -1;
-            levels_out[i].min_ped = cnt > 0 ? pool[0].ped : -1;
+            levels_out[i].threshold = (cnt > K) ? mx : -1; /* PED of the K-th smallest key */
+            levels_out[i].min_ped = mn;
         }
         /* Next frontier in canonical (p, j) order (C13). */
         qsort(pool, (size_t)keep, sizeof(cand), cmp_pos);
@@ -322,6 +353,27 @@ int og_max_threads(void) {
 #else
     return 1;
 #endif
+}
+
+/* Exposed for the selection pin: indices of the k smallest keys
+ * (ped[x], p[x], j[x]) as chosen by select_k, ascending by index. */
+int og_select(const int64_t *ped, const int64_t *p, const int32_t *j, int64_t n, int64_t k, int64_t *idx_out) {
+    if (n < 0 || k < 0 || (n > 0 && (!ped || !p || !j || !idx_out))) return OG_ERR_ARG;
+    cand *a = (cand *)malloc(sizeof(cand) * (size_t)(n > 0 ? n : 1));
+    char *take = (char *)calloc((size_t)(n > 0 ? n : 1), 1);
+    if (!a || !take) { free(a); free(take); return OG_ERR_MEM; }
+    for (int64_t x = 0; x < n; x++) { a[x].ped = ped[x]; a[x].p = p[x]; a[x].j = j[x]; }
+    int64_t keep = k < n ? k : n;
+    select_k(a, n, keep);
+    /* map each selected key back to its input index (keys are unique) */
+    for (int64_t s = 0; s < keep; s++)
+        for (int64_t x = 0; x < n; x++)
+            if (!take[x] && a[s].ped == ped[x] && a[s].p == p[x] && a[s].j == j[x]) { take[x] = 1; break; }
+    int64_t c = 0;
+    for (int64_t x = 0; x < n; x++)
+        if (take[x]) idx_out[c++] = x;
+    free(a); free(take);
+    return c == keep ? OG_OK : OG_ERR_ARG;
 }
 
 /* Exposed for the witness tests: order-free cost of a given complete mapping. */

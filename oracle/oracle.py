@@ -12,7 +12,8 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# FASTGED_ORACLE_LIB: a mutated build for scripts/oracle_mutations.py (never set otherwise)
+LIB_PATH = os.environ.get("FASTGED_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
 SRC_PATH = os.path.join(_HERE, "fastged_oracle.c")
 
 
@@ -41,6 +42,8 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc -O2 -fopenmp).  Building the checker is not using it."""
+    if os.environ.get("FASTGED_ORACLE_LIB"):
+        return LIB_PATH
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(SRC_PATH):
         tmp = LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared", "-Wall",
@@ -67,6 +70,8 @@ def lib():
                                       C.c_void_p, C.POINTER(C.c_int64)]
         L.og_mapping_cost.restype = C.c_int
         L.og_max_threads.restype = C.c_int
+        L.og_select.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
+        L.og_select.restype = C.c_int
         _lib = L
     return _lib
 
@@ -140,6 +145,17 @@ def mapping_cost(g1, g2, costs, mapping) -> int:
     if rc != 0:
         raise OracleError(rc)
     return int(out.value)
+
+
+def select(ped, p, j, k) -> np.ndarray:
+    """Indices (ascending) of the k smallest keys (ped, p, j) as the oracle's selection step picks them."""
+    ped, p, j = _arr(ped, np.int64), _arr(p, np.int64), _arr(j, np.int32)
+    n = int(ped.shape[0])
+    out = np.zeros(max(min(int(k), n), 1), np.int64)
+    rc = lib().og_select(ped.ctypes.data, p.ctypes.data, j.ctypes.data, n, int(k), out.ctypes.data)
+    if rc != 0:
+        raise OracleError(rc)
+    return out[:min(int(k), n)].copy()
 
 
 def max_threads() -> int:

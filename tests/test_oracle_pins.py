@@ -84,6 +84,57 @@ def test_hand_traces_k1(oracle_lib, case):
     assert r["mapping"].tolist() == case["mapping"]
 
 
+def _k2_cases():
+    with open(os.path.join(GOLD, "hand_traces_k2.json")) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", _k2_cases(), ids=lambda c: c["name"])
+def test_hand_traces_k2(oracle_lib, case):
+    """K >= 2 hand traces that pin the two readings the K = 1 traces cannot see:
+    C13 (survivors re-ordered by (p, j)) and C10 (last level ranked by PED, completion after)."""
+    from oracle import bruteforce
+    g1, g2 = _g(case["g1"]), _g(case["g2"])
+    r = oracle_lib.kbest(g1, g2, case["costs"], case["K"], levels=True)
+    assert r["cost"] == case["cost"], case["name"]
+    assert r["mapping"].tolist() == case["mapping"], case["name"]
+    assert [list(x) for x in r["levels"]] == case["levels"], case["name"]
+    # the pinned value is an upper bound of the exact GED, and its witness re-verifies
+    assert r["cost"] >= bruteforce.exact_ged(g1, g2, case["costs"])[0]
+    assert int(bruteforce.costs_of(g1, g2, case["costs"], r["mapping"][None, :])[0]) == r["cost"]
+
+
+def test_selection_examples(oracle_lib):
+    """P5: the selection step keeps the k smallest unique keys."""
+    sel = oracle_lib.select
+    # [5,1,3,2,4], k=2 -> {1,2} (the values at indices 1 and 3)
+    assert sel([5, 1, 3, 2, 4], [0] * 5, [0, 1, 2, 3, 4], 2).tolist() == [1, 3]
+    # k >= size -> everything
+    assert sel([5, 1, 3], [0] * 3, [0, 1, 2], 7).tolist() == [0, 1, 2]
+    # equal PEDs: the smaller tag wins ([1,1,1] with tags 0,1,2, k=2 -> {0,1})
+    assert sel([1, 1, 1], [0, 0, 0], [0, 1, 2], 2).tolist() == [0, 1]
+    # ties broken by parent before child (C12)
+    assert sel([3, 3, 3, 1], [2, 0, 1, 9], [0, 5, 4, 0], 3).tolist() == [1, 2, 3]
+    assert sel([], [], [], 3).tolist() == []
+
+
+def test_selection_equals_full_sort(oracle_lib):
+    """P5: quickselect and a full sort by (PED, p, j) pick the same set (keys are unique), on
+    random pools shaped like a level (few distinct PEDs, many ties, every k)."""
+    rng = synth.rng_for(515)
+    for trial in range(300):
+        n = int(rng.integers(1, 400))
+        npar = int(rng.integers(1, 40))
+        p = rng.integers(0, npar, size=n)
+        j = rng.permutation(n).astype(np.int32)  # unique (p, j) keys
+        ped = rng.integers(0, int(rng.integers(1, 12)), size=n)
+        k = int(rng.integers(0, n + 3))
+        order = np.lexsort((j, p, ped))
+        want = np.sort(order[:min(k, n)])
+        got = oracle_lib.select(ped, p, j, k)
+        assert np.array_equal(got, want), (trial, n, k)
+
+
 def test_empty_graph_closed_forms(oracle_lib):
     """n1 = 0 -> vins*n2 + eins*m2; n2 = 0 -> vdel*n1 + edel*m1 (S:236, C16)."""
     c = COSTS["setting1"]
