@@ -36,22 +36,41 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _stamp(flags) -> str:
+    """What the in-tree library was built from: the nvcc flags (an A/B or debug build must never be
+    mistaken for the product build)."""
+    return " ".join(flags)
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    if any(os.path.getmtime(d) > t for d in DEPS):
+        return True
+    try:
+        with open(LIB + ".flags") as f:
+            return f.read() != _stamp(NVCC_FLAGS)
+    except OSError:
+        return True
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+def build(force: bool = False, verbose: bool = False, out: str = None, extra_flags=()) -> str:
+    """Build the product library in-tree (LIB), or -- with `out` -- a variant with `extra_flags`
+    (A/B or debug builds) at `out`, leaving the in-tree library untouched."""
+    flags = list(NVCC_FLAGS) + list(extra_flags)
+    if out is None:
+        if extra_flags:
+            raise ValueError("variant builds need an output path outside the package")
+        if not force and not stale():
+            return LIB
+    target = out or LIB
+    tmp = target + f".tmp{os.getpid()}"
     nd = nccl_dir()
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-o", tmp, *SRCS,
+    cmd = [nvcc(), *flags, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-o", tmp, *SRCS,
            "-lcudart", "-lgomp", "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "csrc", "ptxas.log")
+    log = os.path.join(HERE, "csrc", "ptxas.log") if out is None else target + ".ptxas.log"
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
@@ -59,8 +78,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libfastged.so (see %s)" % log)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    if out is None:
+        with open(LIB + ".flags", "w") as f:
+            f.write(_stamp(flags))
+    return target
 
 
 if __name__ == "__main__":

@@ -8,6 +8,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -25,9 +28,16 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// Device allocation owned by its holder (freed on destruction, so an error thrown mid-call
+// cannot leak it); not copyable.
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    DevBuf(DevBuf &&o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+    ~DevBuf() { release(); }
     cudaError_t reserve(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
@@ -48,6 +58,10 @@ struct DevBuf {
 struct HostPinned {
     void *p = nullptr;
     size_t cap = 0;
+    HostPinned() = default;
+    HostPinned(const HostPinned &) = delete;
+    HostPinned &operator=(const HostPinned &) = delete;
+    ~HostPinned() { release(); }
     cudaError_t reserve(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFreeHost(p);
@@ -189,9 +203,36 @@ void check_overflow(const fastged_graph_t *g1, const fastged_graph_t *g2, const 
         fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", pair, (long long)bound);
 }
 
-// Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024, K <= 2^24.
-bool fits_batched(const fastged_graph_t *g1, const fastged_graph_t *g2, int64_t k) {
-    return g2->n <= 128 && g1->n <= 1024 && k <= (1 << 24); // (n1 <= 1024: P_{i+1} membership bitmask)
+// Largest frontier any level can hold: N_{i+1} <= min(K, N_i (n2 + 1)), N_0 = 1.  When K exceeds
+// the returned cap, no level has more than cap candidates, so K and the cap select identically.
+int64_t frontier_cap(int n1, int n2, int64_t k) {
+    int64_t N = 1, mx = 1;
+    for (int i = 0; i < n1 && N < k; ++i) {
+        N = std::min<int64_t>(k, N * (int64_t)(n2 + 1));
+        mx = std::max(mx, N);
+    }
+    return std::min(mx, k);
+}
+
+// Per-CTA bytes of the batched kernel's per-level work arrays (the layout run_batch plans), in 64 bits.
+size_t batched_work_bytes(int64_t Kc, int W, int csmax, bool lab) {
+    auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    return a16(4 * (size_t)Kc * W) + a16(4 * (size_t)(Kc + 1)) + (lab ? a16((size_t)fg::DMAX * Kc) : 0) +
+           a16((size_t)Kc * csmax) + a16(4 * (size_t)Kc) + a16(2 * ((size_t)Kc * csmax / 16 + 2));
+}
+
+// Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024 (P_{i+1} membership bitmask),
+// and every 32-bit offset of the plan fits: the codes of one level (Kc * csmax bytes, indexed with
+// int32 in the kernel) and the work arrays stay below 2^31 with room to spare.  csmax is taken at the
+// top of the pair's word-width bucket (the group's plan uses the bucket maximum).  Pairs beyond the
+// limits are solved by the whole-GPU kernel (solve_large), inside a batch as well.
+bool fits_batched(int n1, int n2, int64_t k) {
+    if (n2 > 128 || n1 > 1024) return false;
+    const int W = words_for(n2);
+    const int64_t Kc = (frontier_cap(n1, n2, k) + 3) & ~3ll;
+    const int csmax = (32 * W + 1 + 3) & ~3;
+    const int64_t lim = ((int64_t)1 << 31) - ((int64_t)1 << 24);
+    return Kc * csmax < lim && (int64_t)batched_work_bytes(Kc, W, csmax, true) < lim;
 }
 
 // ---------------------------------------------------------------- packing
@@ -343,6 +384,9 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
             } catch (const FgError &e) {
 #pragma omp critical(fg_err)
                 if (p < bad) { bad = p; perr[0] = e; }
+            } catch (...) { // (std::bad_alloc) no exception may leave the parallel region
+#pragma omp critical(fg_err)
+                if (p < bad) { bad = p; perr[0] = FgError{FASTGED_ERR_CAPACITY, "pair " + std::to_string(pair_base + p) + ": host allocation failed"}; }
             }
         }
         if (bad < npairs) throw perr[0];
@@ -366,6 +410,9 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
             } catch (const FgError &e) {
 #pragma omp critical(fg_err)
                 if (p < bad) { bad = p; perr[0] = e; }
+            } catch (...) {
+#pragma omp critical(fg_err)
+                if (p < bad) { bad = p; perr[0] = FgError{FASTGED_ERR_CAPACITY, "pair " + std::to_string(pair_base + p) + ": host allocation failed"}; }
             }
             b->descs[p].map_out = b->map_off[p];
             b->W[p] = words_for(g2s[p].n);
@@ -395,16 +442,6 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
     }
 }
 
-// Largest frontier any level can hold: N_{i+1} <= min(K, N_i (n2 + 1)), N_0 = 1.
-int64_t frontier_cap(int n1, int n2, int64_t k) {
-    int64_t N = 1, mx = 1;
-    for (int i = 0; i < n1 && N < k; ++i) {
-        N = std::min<int64_t>(k, N * (int64_t)(n2 + 1));
-        mx = std::max(mx, N);
-    }
-    return std::min(mx, k);
-}
-
 #ifndef FG_BATCH_NT
 #define FG_BATCH_NT 256
 #endif
@@ -422,6 +459,52 @@ void *batch_kernel_for(int W, bool lab, bool smem) {
     return nullptr;
 }
 
+// Device destinations of one pair's results inside a batch (solve_large writes there instead of
+// returning to the host).
+struct LargeDst {
+    int64_t *cost, *children, *parents, *algb;
+    int32_t *map;
+};
+void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
+                 const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
+                 const LargeDst *dst = nullptr);
+
+// A pair rebuilt from its packed form in the batch's staging (vertex labels as given, edge labels
+// as the interned ids of pack_pair -- equal ids exactly where the original labels are equal, which is
+// all the costs depend on).  Used to hand a pair beyond the batched limits to solve_large.
+struct HostGraph {
+    std::vector<int32_t> vl, e, el;
+    fastged_graph_t view() const {
+        return fastged_graph_t{(int32_t)vl.size(), (int32_t)(e.size() / 2), vl.data(), e.data(), el.data()};
+    }
+};
+void unpack_pair(const uint8_t *stage, const fg::PairDesc &d, HostGraph &g1, HostGraph &g2) {
+    const int32_t *vl1 = (const int32_t *)(stage + d.vl1), *vl2 = (const int32_t *)(stage + d.vl2);
+    const int32_t *pptr = (const int32_t *)(stage + d.pptr), *pq = (const int32_t *)(stage + d.pq);
+    const int32_t *pl = (const int32_t *)(stage + d.pl);
+    const uint32_t *adj2 = (const uint32_t *)(stage + d.adj2);
+    const uint8_t *e2 = d.labelled ? stage + d.e2lab : nullptr;
+    const int W = words_for(d.n2);
+    g1.vl.assign(vl1, vl1 + d.n1);
+    g2.vl.assign(vl2, vl2 + d.n2);
+    g1.e.clear(); g1.el.clear(); g2.e.clear(); g2.el.clear();
+    for (int i = 0; i < d.n1; ++i)
+        for (int x = pptr[i]; x < pptr[i + 1]; ++x) {
+            g1.e.push_back(pq[x]);
+            g1.e.push_back(i);
+            g1.el.push_back(pl[x]);
+        }
+    for (int u = 0; u < d.n2; ++u)
+        for (int v = u + 1; v < d.n2; ++v)
+            if ((adj2[(size_t)u * W + (v >> 5)] >> (v & 31)) & 1u) {
+                g2.e.push_back(u);
+                g2.e.push_back(v);
+                g2.el.push_back(e2 ? (int32_t)e2[(size_t)u * d.n2p + v] : 0);
+            }
+    g1.el.push_back(0); // (non-empty: .data() is a valid pointer for m = 0)
+    g2.el.push_back(0);
+}
+
 // first = false appends to the timing/launch stats of a preceding run_batch on the same stream
 // (pipelined chunks of one solve_batch call).
 void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, int64_t k,
@@ -437,14 +520,11 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
                         ((int64_t)d.m1 + d.m2) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
         if (bound >= ((int64_t)1 << 31))
             fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
-        if (d.n2 <= 128 && d.n1 <= 1024 && k <= (1 << 24))
+        if (fits_batched(d.n1, d.n2, k) && !(h->flags & FASTGED_FLAG_FORCE_LARGE))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
-            b->large.push_back(p);
+            b->large.push_back(p); // solved by the whole-GPU kernel after the batched launches
     }
-    if (!b->large.empty())
-        fail(FASTGED_ERR_CAPACITY, "pair %d exceeds the batched limits (n2 <= 128, n1 <= 1024, k <= 2^24); "
-                                   "solve it with fastged_solve_pair", b->pair_base + b->large[0]);
     if (first) {
         h->evused = 0;
         h->stats.kernel_launches = 0;
@@ -493,7 +573,9 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.blob = (const uint8_t *)b->blob.p;
         a.work = (int32_t *)b->dwork.p + gi;
         a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
-        a.K = (int)k;
+        // k beyond every level's candidate count selects like the cap (frontier_cap), so the kernel's
+        // int32 K is min(k, cap)
+        a.K = (int)std::min<int64_t>(k, kcap);
         a.Kc = (int)((kcap + 3) & ~3ll);
         a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 127; // codes 0..128 (SWAR compares need <= 128)
         a.n1max = std::max(4, (n1max + 3) & ~3);
@@ -606,6 +688,24 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             CK(cudaStreamWaitEvent(h->stream, h->gevents[g], 0));
         }
     }
+    // pairs beyond the batched limits: the whole-GPU kernel, one pair after the other on the handle's
+    // stream, results written into this batch's device outputs (SURVEY §3.3 size classes)
+    for (size_t x = 0; x < b->large.size(); ++x) {
+        const int p = b->large[x];
+        const fg::PairDesc &d = b->descs[p];
+        HostGraph G1, G2;
+        unpack_pair((const uint8_t *)b->stage.p, d, G1, G2);
+        const fastged_graph_t v1 = G1.view(), v2 = G2.view();
+        if (x > 0) CK(cudaStreamSynchronize(h->stream)); // solve_large restages through h->stage
+        LargeDst dst{(int64_t *)b->dcost.p + p, (int64_t *)b->dchild.p + p, (int64_t *)b->dpar.p + p,
+                     (int64_t *)b->dalg.p + p, (int32_t *)b->dmap.p + b->map_off[p]};
+        try {
+            solve_large(h, &v1, &v2, c, k, nullptr, nullptr, &dst);
+        } catch (FgError &e) {
+            e.msg = "pair " + std::to_string(b->pair_base + p) + " (whole-GPU path): " + e.msg;
+            throw;
+        }
+    }
     CK(cudaEventRecord(h->ev_end, h->stream));
     b->ran = true;
 }
@@ -688,7 +788,8 @@ void begin_call(fastged_handle_t *h) {
 
 
 void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
-                 const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out) {
+                 const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
+                 const LargeDst *dst) {
     const int n1 = g1->n, n2 = g2->n;
     if (n2 > FASTGED_MAX_N2) fail(FASTGED_ERR_CAPACITY, "target graph has n2=%d > %d (limit of this build)", n2, FASTGED_MAX_N2);
     const int64_t Kc64 = frontier_cap(n1, n2, k);
@@ -836,11 +937,29 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.out = (int64_t *)(B + o_out);
     a.map_out = (int32_t *)(B + o_mapout);
     a.levels_out = levels_out ? (int64_t *)(B + o_lev) : nullptr;
+    void *params[] = {(void *)&a};
+    if (dst) { // inside a batch: enqueue only, results stay on the device (stream-ordered copies)
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (h->flags & FASTGED_FLAG_TIMING) {
+            e0 = next_event(h);
+            e1 = next_event(h);
+            CK(cudaEventRecord(e0, h->stream));
+        }
+        CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(fg::LNT), params, smem, h->stream));
+        if (e1) CK(cudaEventRecord(e1, h->stream));
+        h->stats.kernel_launches++;
+        int64_t *res = a.out; // [cost, children, parents, alg_bytes, ...]
+        CK(cudaMemcpyAsync(dst->cost, res + 0, 8, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(dst->children, res + 1, 8, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(dst->parents, res + 2, 8, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(dst->algb, res + 3, 8, cudaMemcpyDeviceToDevice, h->stream));
+        if (n1) CK(cudaMemcpyAsync(dst->map, a.map_out, 4 * (size_t)n1, cudaMemcpyDeviceToDevice, h->stream));
+        return;
+    }
     h->evused = 0;
     cudaEvent_t e0 = next_event(h), e1 = next_event(h);
     CK(cudaEventRecord(h->ev_begin, h->stream));
     CK(cudaEventRecord(e0, h->stream));
-    void *params[] = {(void *)&a};
     CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(fg::LNT), params, smem, h->stream));
     CK(cudaEventRecord(e1, h->stream));
     CK(cudaEventRecord(h->ev_end, h->stream));
@@ -1102,7 +1221,7 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
             solve_sharded(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }
-        if (!fits_batched(g1, g2, k) || (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
+        if (!fits_batched(g1->n, g2->n, k) || (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }

@@ -343,13 +343,4 @@ __global__ void reduce_totals(const int32_t *wlt, const int32_t *weq, int n, int
     }
 }
 
-// Element-wise sum of G device arrays (loopback all-reduce of the virtual-shard mode).
-__global__ void sh_sum_i32(int32_t *const *src, int G, int n, int32_t *dst) {
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-        int s = 0;
-        for (int g = 0; g < G; ++g) s += src[g][x];
-        dst[x] = s;
-    }
-}
-
 } // namespace fg

@@ -1,8 +1,4 @@
+# window-2 repro against a -DFG_DEBUG_CHECKS variant (ab/debug.so; the in-tree library is untouched)
 cd $GRAFT_REPO_ROOT
-NVCC_EXTRA="-DFG_DEBUG_CHECKS" python -c "
-import os
-from paper_2605_00830_b200 import build
-build.NVCC_FLAGS.append('-DFG_DEBUG_CHECKS')
-build.build(force=True)
-"
-timeout 300 python scripts/repro_window2.py 2>&1 | head -40
+python scripts/ab_build.py debug -DFG_DEBUG_CHECKS > /dev/null
+FASTGED_LIB=ab/debug.so timeout 300 python scripts/repro_window2.py 2>&1 | head -40

@@ -30,18 +30,27 @@ def _worker(rank, world, port, q):
         from oracle import oracle
         from paper_2605_00830_b200 import dist as fdist
         from paper_2605_00830_b200 import synth
+        from paper_2605_00830_b200 import binding
         w = synth.config_workload(3, npairs=11, K=40)
-        idx = fdist.shard_pairs(w.npairs, rank, world)
-        pairs = [w.pair(int(k)) for k in idx]
-        c, maps, _ = oracle.kbest_batch(pairs, w.costs, w.K, nthreads=1)
-        offs = np.concatenate([[0], np.cumsum([m.shape[0] for m in maps])]).astype(np.int64)
-        flat = np.concatenate(maps + [np.zeros(0, np.int32)]).astype(np.int32)
-        res = fdist.gather_results(w.npairs, idx, c, flat, offs,
-                                   [w.pair(k)[0].n for k in range(w.npairs)])
+        packed = binding.PackedGraphs(w.graphs)
+        seen = []
+
+        class OracleSolver:  # stands in for binding.Handle (the per-rank GPU search) on a CPU box
+            def solve_batch(self, pk, a, b, costs, K):
+                seen.extend(int(x) // 2 for x in a)
+                pairs = [(w.graphs[int(x)], w.graphs[int(y)]) for x, y in zip(a, b)]
+                c, maps, ch = oracle.kbest_batch(pairs, costs, K, nthreads=1)
+                offs = np.concatenate([[0], np.cumsum([m.shape[0] for m in maps])]).astype(np.int64)
+                flat = np.concatenate(maps + [np.zeros(0, np.int32)]).astype(np.int32)
+                return c, flat, offs, ch
+
+        res = fdist.solve_batch_sharded(OracleSolver(), packed, w.pair_a, w.pair_b, w.costs, w.K)
+        assert seen == list(range(rank, w.npairs, world))  # pair r -> rank r mod world
         uid = fdist.nccl_id_for_group()
         ids = [None] * world
         dist.all_gather_object(ids, uid)
-        q.put((rank, None if res is None else (res[0].tolist(), [m.tolist() for m in res[1]]),
+        q.put((rank, None if res is None else
+               (res[0].tolist(), [res[1][res[2][k]:res[2][k + 1]].tolist() for k in range(w.npairs)]),
                len(uid), all(x == ids[0] for x in ids)))
     finally:
         dist.destroy_process_group()

@@ -110,25 +110,85 @@ def test_config3_er_grid_sampled(fg, handle, oracle):
     assert_batch_parity(fg, handle, oracle, pairs, w.costs, w.K, "cfg3")
 
 
-def test_config3_full_launch_sampled_outputs(fg, handle, oracle):
-    """Full 10k-pair config-3 batch (the bench workload); every 250th pair checked against the oracle."""
+def _golden(name):
+    f = os.path.join(os.path.dirname(__file__), "golden", name)
+    if not os.path.exists(f):
+        pytest.fail(f"{f} missing: run scripts/make_golden.py (oracle results at full size)")
+    return np.load(f)
+
+
+def assert_golden(z, gc, gm, goffs, gch, label):
+    """GPU results of the pairs z['idx'] against the oracle's stored results, element by element."""
+    idx, oc, om, oo, och = z["idx"], z["cost"], z["map"], z["offs"], z["children"]
+    bad = [x for x in range(idx.shape[0])
+           if gc[idx[x]] != oc[x] or gch[idx[x]] != och[x]
+           or not np.array_equal(gm[goffs[idx[x]]:goffs[idx[x] + 1]], om[oo[x]:oo[x + 1]])]
+    assert not bad, f"{label}: {len(bad)} of {idx.shape[0]} pairs differ from the oracle, first pair {idx[bad[0]]}"
+    return idx.shape[0]
+
+
+def test_config3_full_batch_vs_golden(fg, handle):
+    """configs[2], the bench workload: all 10,000 pairs in the launch configuration bench.py times,
+    bit-exact against the oracle's results for every pair (tests/golden/oracle_cfg3.npz)."""
     w = synth.config_workload(3)
     packed = fg.PackedGraphs(w.graphs)
     gc, gm, offs, gch = handle.solve_batch(packed, w.pair_a, w.pair_b, w.costs, w.K)
-    idx = list(range(0, w.npairs, 250))
-    pairs = [w.pair(k) for k in idx]
-    oc, om, och = oracle.kbest_batch(pairs, w.costs, w.K, nthreads=NCPU)
-    for x, k in enumerate(idx):
-        assert gc[k] == oc[x] and np.array_equal(gm[offs[k]:offs[k + 1]], om[x]) and gch[k] == och[x], k
+    assert assert_golden(_golden("oracle_cfg3.npz"), gc, gm, offs, gch, "cfg3") == 10_000
+    # the device-resident path bench.py times gives the same results
+    b = handle.upload(packed, w.pair_a, w.pair_b)
+    b.run(w.costs, w.K)
+    r = b.download()
+    b.free()
+    assert np.array_equal(r[0], gc) and np.array_equal(r[1], gm)
 
 
-def test_config5_muta_like_sampled(fg, handle, oracle):
-    """configs[4]: Mutagenicity-like all-pairs, Setting 1 and Setting 2, K=1000 — a strided subset."""
-    w = synth.config_workload(5, npairs=400_000)
-    idx = np.arange(0, w.npairs, 4000)
-    pairs = [w.pair(int(k)) for k in idx]
-    assert_batch_parity(fg, handle, oracle, pairs, w.costs, w.K, "cfg5-s1")
-    assert_batch_parity(fg, handle, oracle, pairs[:40], COSTS["setting2"], w.K, "cfg5-s2")
+@pytest.mark.parametrize("setting", ["s1", "s2"])
+def test_config5_allpairs_vs_golden(fg, handle, setting):
+    """configs[4]: the full 1,999,000-pair all-pairs batch in one call (Setting 1 and Setting 2);
+    every 100th pair (19,990) bit-exact against the oracle (tests/golden/oracle_cfg5_*.npz)."""
+    w = synth.config_workload(5, variant=None if setting == "s1" else "setting2")
+    packed = fg.PackedGraphs(w.graphs)
+    gc, gm, offs, gch = handle.solve_batch(packed, w.pair_a, w.pair_b, w.costs, w.K)
+    assert gc.shape[0] == 1_999_000 and (gc >= 0).all()
+    assert assert_golden(_golden(f"oracle_cfg5_{setting}.npz"), gc, gm, offs, gch, f"cfg5-{setting}") == 19_990
+
+
+def test_batched_frontier_beyond_65535(fg, handle, oracle):
+    """K = 70,000 on small pairs: the frontier capacity exceeds 65,535, so the batched kernel keeps
+    its work arrays in global scratch and decodes survivor positions by binary search over the parent
+    offsets (batch_kernel.cuh decode, Kc > 65535 branch)."""
+    rng = synth.rng_for(70)
+    pairs = []
+    for k in range(6):
+        n1, n2 = int(rng.integers(6, 9)), int(rng.integers(9, 14))
+        pairs.append((synth.er_graph(rng, n1, 0.4, 3), synth.er_graph(rng, n2, 0.4, 3)))
+    assert_batch_parity(fg, handle, oracle, pairs, COSTS["setting1"], 70_000, "K=70000")
+
+
+def test_oversize_pairs_routed_inside_a_batch(fg, handle, oracle):
+    """Pairs beyond the batched limits (n2 in {150, 300}) inside one fastged_solve_batch call are solved
+    by the whole-GPU kernel and land in the same outputs; the rest of the batch is unaffected."""
+    small = [synth.config_workload(3, npairs=6, K=300).pair(k) for k in range(6)]
+    big = [synth.large_pair(150, 0.1, seed=3), synth.large_pair(300, 0.05, seed=5)]
+    pairs = [small[0], big[0], small[1], small[2], big[1], small[3]]
+    assert_batch_parity(fg, handle, oracle, pairs, COSTS["setting1"], 300, "mixed sizes")
+
+
+def test_frontier_2_24_with_128_targets(fg, handle, oracle):
+    """K = 2^24 with n2 = 128: the batched plan's 32-bit offsets would wrap (Kc * csmax
+    > 2^31), so the pair must go to the whole-GPU kernel, inside a batch too; the result equals the
+    oracle's (2.7e8 candidates at the last level, 2^24 kept)."""
+    rng = synth.rng_for(24)
+    g1 = synth.er_graph(rng, 4, 0.5, 2)
+    g2 = synth.er_graph(rng, 128, 0.02, 2)
+    K = 1 << 24
+    o = oracle.kbest(g1, g2, COSTS["setting1"], K)
+    r = handle.solve_pair(g1, g2, COSTS["setting1"], K)
+    assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]) and r["children"] == o["children"]
+    small = (synth.path_graph(3), synth.cycle_graph(4))
+    gc, gm, gch = gpu_batch(fg, handle, [(g1, g2), small], COSTS["setting1"], K)
+    assert gc[0] == o["cost"] and np.array_equal(gm[0], o["mapping"])
+    assert gc[1] == oracle.kbest(*small, COSTS["setting1"], K)["cost"]
 
 
 # ------------------------------------------------------------------ per-level parity
@@ -217,21 +277,33 @@ def test_large_pairs(fg, handle, oracle, n, p, K):
     assert r["levels"] == [tuple(x) for x in o["levels"]]
 
 
-def test_config4_n200_k1e4(fg, handle, oracle):
-    """configs[3] corner n=200, p=0.2, K=1e4 (and p=0.05): full parity with the oracle."""
+def _cfg4_golden():
+    import json
+    f = os.path.join(os.path.dirname(__file__), "golden", "oracle_cfg4.json")
+    return json.load(open(f))["runs"] if os.path.exists(f) else {}
+
+
+@pytest.mark.parametrize("idx", range(8), ids=lambda k: "({},{},{})".format(*synth.config_workload(4).run_np[k]))
+def test_config4_corners_vs_golden(fg, handle, idx):
+    """configs[3]: every single-pair corner n in {200, 500} x p in {0.05, 0.2} x K in {1e4, 1e5}
+    (the bench pair is (500, 0.05, 1e5)) bit-exact against the oracle's stored result: cost, mapping,
+    children evaluated and every level's (N_i, c_i, threshold) (tests/golden/oracle_cfg4.json)."""
+    runs = _cfg4_golden()
+    if str(idx) not in runs:
+        pytest.fail("tests/golden/oracle_cfg4.json lacks this corner: run scripts/make_golden.py cfg4")
+    o = runs[str(idx)]
     w = synth.config_workload(4)
-    for idx in (0, 2):  # (200, .05, 1e4), (200, .2, 1e4)
-        g1, g2 = w.pair(idx)
-        K = w.run_K[idx]
-        r = handle.solve_pair(g1, g2, w.costs, K)
-        o = oracle.kbest(g1, g2, w.costs, K)
-        assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]) and r["children"] == o["children"]
+    g1, g2 = w.pair(idx)
+    r = handle.solve_pair(g1, g2, w.costs, o["K"], levels=True)
+    assert r["cost"] == o["cost"] and r["mapping"].tolist() == o["mapping"]
+    assert r["children"] == o["children"] and r["parents"] == o["parents"]
+    assert [list(x) for x in r["levels"]] == o["levels"]
 
 
-def test_config4_n500_properties(fg, handle):
-    """configs[3] corner n=500, K=1e5: beyond the oracle's budget; check what holds at any size —
-    the witness re-verifies with the order-free cost, the mapping is injective, and the cost is
-    within [lower bound, cost of the identity-order greedy K=1 run]."""
+def test_config4_n500_witness(fg, handle):
+    """configs[3] bench pair (n=500, p=0.05, K=1e5): the returned mapping is injective and its
+    order-free cost (O.4) equals the returned cost.  (No monotonicity in K is asserted: per-pair
+    monotonicity is not guaranteed, SPEC S:247 / SURVEY C25.)"""
     from oracle import oracle as o
     w = synth.config_workload(4)
     g1, g2 = w.pair(5)  # (500, 0.05, 1e5)
@@ -240,8 +312,6 @@ def test_config4_n500_properties(fg, handle):
     used = m[m >= 0]
     assert len(set(used.tolist())) == used.size and (used < g2.n).all()
     assert o.mapping_cost(g1, g2, w.costs, m) == r["cost"]
-    r1 = handle.solve_pair(g1, g2, w.costs, 1)
-    assert r["cost"] <= r1["cost"]
 
 
 # ------------------------------------------------------------------ errors
