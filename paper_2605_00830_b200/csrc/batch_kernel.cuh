@@ -15,8 +15,9 @@
 //          Delta(u)   = cv(i,u) + edel*d_i + eins*cnt_p(u) - (edel+eins)*cB_p(u) + esub*mis_p(u)
 //          Delta(DEL) = vdel + edel*d_i
 //      cnt_p(u) = popc(adj2[u] & used_p), cB_p(u) = popc(adj2[u] & B_p), B_p = images of the earlier
-//      g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors); labelled edges
-//      compare the edge labels of (u, t_k) per earlier neighbour (mis_p).  Wide frontiers: a thread
+//      g1 neighbours of v_i (replaces the paper's VFrom/VTo vectors); labelled edges:
+//      mis_p(u) = cB_p(u) - sum_l popc(adj2_l[u] & B_{p,l}), one g2 label plane adj2_l per edge label and
+//      B_{p,l} = the images whose g1 edge to v_i has label l (kept per node like B_p).  Wide frontiers: a thread
 //      per parent iterates only that parent's free targets; narrow ones: a warp per parent with
 //      lane-owned targets.  Each child becomes a one-byte rank code (PED - base + 1, saturated) in
 //      shared memory and one atomic in its warp's private 128-bin histogram.  Children never reach HBM.
@@ -29,7 +30,7 @@
 //      are written as (parent, rank within parent) in (parent, child) order (C13), then decoded to
 //      (p, j) and their PED (from the rank code) in a balanced pass.
 //   U  Update: next frontier columns with coalesced stores; while copying the
-//      lambda columns, B_p of the next level is accumulated (no separate gathers).
+//      lambda columns, B_p (and the label planes B_{p,l}) of the next level are accumulated.
 // After the last level each survivor gets the insertion completion (C6) and the
 // argmin by (total, position) is written out (C10).
 #pragma once
@@ -45,7 +46,7 @@ namespace fg {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAP_DEL = 255;      // lambda entry of a deleted g1 vertex
 constexpr int CODE_INVALID = 255; // no child in this slot (used target / padding)
-constexpr int DMAX = 8;           // labelled path: lambda images of P_i staged per parent
+constexpr int LMAX = 3;           // edge-label planes of the batched path (more labels: whole-GPU path)
 
 struct Costs {
     int vsub, vdel, vins, esub, edel, eins;
@@ -55,6 +56,7 @@ struct Costs {
 struct PairDesc {
     int32_t n1, n2, m1, m2;
     int32_t labelled, n2p;       // n2p: row stride of the e2lab byte matrix (multiple of 4)
+    int32_t nlab, pad0;          // nlab: distinct g2 edge labels (label ids 1..nlab), labelled pairs
     int64_t vl1, vl2;            // int32[n1], int32[n2]
     int64_t pptr, pq, pl;        // int32[n1+1], int32[m1], int32[m1]  (P_i lists)
     int64_t adj2;                // uint32[n2 * W]
@@ -62,11 +64,11 @@ struct PairDesc {
     int64_t map_out;             // element offset of this pair's mapping in the output array
 };
 
-// Work-array plan of a batched launch.  pq/pl/e2: byte offsets into dynamic shared memory.
-// ped/u/b/t/codes/sel: byte offsets into shared memory (SMEM launches) or into the CTA's global
-// scratch after its two frontier buffers (large-K launches).
+// Work-array plan of a batched launch.  pq/pl/pnl/adj/adjl/adjh: byte offsets into dynamic shared
+// memory.  u/b/codes/sel/pidx: byte offsets into shared memory (SMEM launches) or into the CTA's
+// global scratch after its two frontier buffers (large-K launches).
 struct SmemPlan {
-    int32_t pq, pl, e2, adj, adjh, ped, u, b, t, codes, sel, pidx, bytes;
+    int32_t pq, pl, pnl, pnq, adj, adjl, adjh, u, b, codes, sel, pidx, bytes;
 };
 
 struct BatchArgs {
@@ -139,9 +141,11 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
 // neither the bit index nor the BREV/FLO pair of __ffs (both on the quarter-rate XU pipe, like POPC).
 __host__ __device__ __forceinline__ uint32_t db_slot(uint32_t b) { return (b * 0x077CB531u) >> 27; }
 
-// Row stride (words) of the slot-addressed g2 rows: W adjacency words + the level's vertex cost cv(i, u),
-// padded so a row is one 8- or 16-byte shared load.
-__host__ __device__ constexpr int hrow_stride(int W) { return W + 1 <= 2 ? 2 : (W + 1 <= 4 ? 4 : 8); }
+// Row stride (words) of the slot-addressed g2 rows: W adjacency words, (labelled) LMAX label planes of
+// W words, then the level's vertex cost cv(i, u); padded so a row is whole 8- or 16-byte shared loads.
+__host__ __device__ constexpr int hrow_stride(int W, bool lab) {
+    return lab ? (((W * (1 + LMAX) + 1) + 3) & ~3) : (W + 1 <= 2 ? 2 : (W + 1 <= 4 ? 4 : 8));
+}
 
 __device__ __forceinline__ int rank_code(int ped, int base, int win) {
     const int x = ped - base + 1;
@@ -188,26 +192,29 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
     __shared__ uint32_t s_pnext2[2][32];
     __shared__ unsigned long long s_best;
     constexpr int NW = NT / 32;
+    constexpr int NB = LAB ? 1 + LMAX : 1;        // B planes per node
+    constexpr int HRS = hrow_stride(W, LAB);      // slot-addressed row stride (words)
+    constexpr int CVW = LAB ? W * (1 + LMAX) : W; // word of the row holding cv(i, u)
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Costs c = a.c;
     const int K = a.K, Kc = a.Kc, win = a.win;
 
-    // per-CTA frontier (two buffers): ped[K], usedT[W][K], mapT[n1max][K]
+    // per-CTA frontier (two buffers): ped[K], usedT[W][K], BT[NB][W][K], mapT[n1max][K]
     uint8_t *scr = a.scratch + (int64_t)blockIdx.x * a.scratch_stride;
-    const int64_t fb = (int64_t)Kc * (4 + 8 * W + a.n1max); // bytes per frontier buffer
+    const int64_t fb = (int64_t)Kc * (4 + 4 * W + 4 * W * NB + a.n1max); // bytes per frontier buffer
     // per-level work arrays: shared memory (SMEM) or, for large K, this CTA's global scratch
     uint8_t *wk = SMEM ? dsmem : scr + 2 * fb;
     int32_t *s_pq = reinterpret_cast<int32_t *>(dsmem + a.sm.pq);
     int32_t *s_pl = reinterpret_cast<int32_t *>(dsmem + a.sm.pl);
-    uint8_t *s_e2 = dsmem + a.sm.e2;
-    uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj); // g2 bit rows [n2][W]
-    // the same rows at [32 w + db_slot(bit)][HRS], word W = cv(i, u) of the current level
+    uint8_t *s_pnl = dsmem + a.sm.pnl; // label plane of the g1 edge (v_q, v_{i+1}) for q in P_{i+1} (LAB)
+    int32_t *s_pnq = reinterpret_cast<int32_t *>(dsmem + a.sm.pnq); // P_{i+1} as a list (LAB)
+    uint32_t *sAdj = reinterpret_cast<uint32_t *>(dsmem + a.sm.adj);   // g2 bit rows [n2][W]
+    uint32_t *sAdjL = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjl); // label planes [n2][LMAX][W] (LAB)
+    // the same rows at [32 w + db_slot(bit)][HRS]: W adjacency words, label planes, cv(i, u)
     uint32_t *sAdjH = reinterpret_cast<uint32_t *>(dsmem + a.sm.adjh);
-    constexpr int HRS = hrow_stride(W);
     uint32_t *sU = reinterpret_cast<uint32_t *>(wk + a.sm.u);      // used mask of parent p [W][K]
     int32_t *sOff = reinterpret_cast<int32_t *>(wk + a.sm.b);      // first code of parent p [K+1]
-    uint8_t *sT = wk + a.sm.t;
     uint8_t *codes = wk + a.sm.codes;
     uint32_t *sel = reinterpret_cast<uint32_t *>(wk + a.sm.sel);
     // coarse code position -> parent index: pidx[g] = the parent owning code position 16 g
@@ -215,9 +222,10 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
 
     auto fped = [&](int b) { return reinterpret_cast<int32_t *>(scr + b * fb); };
     auto fused = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + 4 * (int64_t)Kc); };
-    // BT[W][K]: B_p of the level about to be expanded, built by the previous level's update
+    // BT[NB][W][K]: B_p (plane 0) and B_{p,l} (planes 1..LMAX) of the level about to be expanded, built
+    // by the previous level's update
     auto fbt = [&](int b) { return reinterpret_cast<uint32_t *>(scr + b * fb + (int64_t)Kc * (4 + 4 * W)); };
-    auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 8 * W); };
+    auto fmap = [&](int b) { return scr + b * fb + (int64_t)Kc * (4 + 4 * W + 4 * W * NB); };
 
 #ifdef FG_PROF
     long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last_ = clock64();
@@ -256,15 +264,20 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             sAdj[x] = v;
             sAdjH[(32 * (u >> 5) + (int)db_slot(1u << (u & 31))) * HRS + y] = v;
         }
-        if (LAB) {
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(a.blob + pd.e2lab);
-            uint32_t *dst = reinterpret_cast<uint32_t *>(s_e2);
-            for (int x = threadIdx.x; x < n2p * n2p / 4; x += NT) dst[x] = __ldg(src + x);
+        if (LAB) { // label planes: bit v of plane l of row u = edge (u, v) with label id l + 1
+            const uint8_t *e2 = a.blob + pd.e2lab;
+            for (int x = threadIdx.x; x < n2 * LMAX * W; x += NT) {
+                const int u = x / (LMAX * W), r = x - u * (LMAX * W), l = r / W, w = r - l * W;
+                uint32_t v = 0;
+                for (int b = 0; b < 32 && 32 * w + b < n2; ++b) v |= (uint32_t)(__ldg(e2 + u * n2p + 32 * w + b) == l + 1) << b;
+                sAdjL[x] = v;
+                sAdjH[(32 * (u >> 5) + (int)db_slot(1u << (u & 31))) * HRS + W + r] = v;
+            }
         }
         // root node: lambda empty, all of V2 remaining, PED 0
         if (threadIdx.x == 0) fped(0)[0] = 0;
-        if (threadIdx.x < W) {
-            fused(0)[(int64_t)threadIdx.x * Kc] = 0u;
+        if (threadIdx.x < W * NB) {
+            if (threadIdx.x < W) fused(0)[(int64_t)threadIdx.x * Kc] = 0u;
             fbt(0)[(int64_t)threadIdx.x * Kc] = 0u; // P_0 is empty
         }
         int N = 1, lo = 0, cur = 0;
@@ -282,6 +295,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             const uint32_t *PBT = fbt(cur);
             uint32_t *QBT = fbt(cur ^ 1);
             const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
+            const int dn = (LAB && i + 1 < n1) ? __ldg(pptr + i + 2) - __ldg(pptr + i + 1) : 0; // |P_{i+1}|
             // membership of P_{i+1} over q (for the next level's B, built during the update)
             uint32_t *s_pnext = s_pnext2[i & 1];
             for (int x = threadIdx.x; x < 32; x += NT) s_pnext2[(i + 1) & 1][x] = 0u; // used last in level i - 1
@@ -290,12 +304,23 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 for (int k = nb + threadIdx.x; k < ne; k += NT) {
                     const int q = __ldg(pq + k);
                     atomicOr(&s_pnext[q >> 5], 1u << (q & 31));
+                    if (LAB) {
+                        s_pnl[q] = (uint8_t)__ldg(pl + k); // (read only for q in P_{i+1})
+                        s_pnq[k - nb] = q;
+                    }
                 }
             }
             for (int k = threadIdx.x; k < d; k += NT) {
                 s_pq[k] = __ldg(pq + pbeg + k);
                 s_pl[k] = __ldg(pl + pbeg + k);
             }
+            // label planes with a non-empty B_{p,l} at this level (uniform)
+            unsigned lmask = 0;
+            if (LAB)
+                for (int k = 0; k < d; ++k) {
+                    const int l = __ldg(pl + pbeg + k);
+                    if (l >= 1 && l <= LMAX) lmask |= 1u << (l - 1);
+                }
             for (int k = threadIdx.x; k < NW * 132; k += NT) s_hist[k] = 0;
             const int vl1i = __ldg(vl1 + i);
             uint32_t Vm[W], Mm[W]; // existing targets / label mismatches, bit u of word u >> 5
@@ -305,12 +330,13 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 const int l2 = (u < n2) ? __ldg(vl2 + u) : 0;
                 Vm[s] = __ballot_sync(FULL, u < n2);
                 Mm[s] = __ballot_sync(FULL, u < n2 && l2 != vl1i);
-                if (u < n2) sAdjH[(32 * s + (int)db_slot(1u << lane)) * HRS + W] = (l2 != vl1i) ? (uint32_t)c.vsub : 0u;
+                if (u < n2) sAdjH[(32 * s + (int)db_slot(1u << lane)) * HRS + CVW] = (l2 != vl1i) ? (uint32_t)c.vsub : 0u;
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
+            // labelled: PED = ... - (ee - esub) cB - esub * (label matches); unlabelled: - ee cB
+            const int eeB = LAB ? ee - c.esub : ee;
             // P_i list, zeroed histograms, P_{i+1} membership and cv words: visible to A through the
-            // barriers of P's block scan (labelled pairs read P_i in P itself)
-            if (LAB) block_sync();
+            // barriers of P's block scan
             FG_PH(0);
 
             // ---------------- P: parents -> used masks in shared memory, compact code offsets ----------------
@@ -331,10 +357,6 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
 #pragma unroll
                 for (int w = 0; w < W; ++w) sU[w * Kc + p] = PusedT[(int64_t)w * Kc + p];
                 nloc += row_bytes(p);
-                if (LAB) {
-                    const int dd = min(d, DMAX);
-                    for (int k = 0; k < dd; ++k) sT[k * Kc + p] = PmapT[(int64_t)s_pq[k] * Kc + p];
-                }
             }
             int obase, dummy, ci, dummy2;
             block_scan2<NT>(nloc, 0, obase, dummy, ci, dummy2, s_tmp); // ci = candidates of the level
@@ -363,17 +385,19 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 if ((unsigned)(code - 1) < (unsigned)win) atomicAdd(&whist[code], 1);
             };
             for (;;) {
-                if (N >= NT / 2 && (!LAB || d <= DMAX)) {
+                if (N >= NT / 2) {
                     // wide frontier: thread per parent, iterating only the parent's free targets (no idle lanes)
                     for (int p = threadIdx.x; p < N; p += NT) {
                         const int pedp = Pped[p];
-                        uint32_t U[W], B[W];
+                        uint32_t U[W], B[NB][W];
                         // B_p: images of the earlier g1 neighbours of v_i (replaces VFrom/VTo)
 #pragma unroll
-                        for (int w = 0; w < W; ++w) { U[w] = sU[w * Kc + p]; B[w] = LAB ? 0u : PBT[(int64_t)w * Kc + p]; }
-                        int tl[DMAX]; // labelled edges: the images t_k themselves (d <= DMAX)
+                        for (int w = 0; w < W; ++w) U[w] = sU[w * Kc + p];
 #pragma unroll
-                        for (int k = 0; k < DMAX; ++k) tl[k] = (LAB && k < d) ? (int)sT[k * Kc + p] : MAP_DEL;
+                        for (int b = 0; b < NB; ++b)
+#pragma unroll
+                            for (int w = 0; w < W; ++w)
+                                B[b][w] = (b == 0 || ((lmask >> (b - 1)) & 1u)) ? PBT[((int64_t)b * W + w) * Kc + p] : 0u;
                         uint8_t *crow = codes + sOff[p];
                         const int pb = pedp - base + 1 + edd;
                         int r = 0;
@@ -382,7 +406,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             // child for the free target whose bit is lb (lowest set bit of F, no bit index)
                             auto child_code = [&](uint32_t lb) -> int {
                                 const uint32_t *row = sAdjH + (32 * w + (int)db_slot(lb)) * HRS;
-                                uint32_t rv[HRS]; // W row words + cv(i, u), one vector load
+                                uint32_t rv[HRS]; // W row words (+ label planes) + cv(i, u), vector loads
                                 if constexpr (HRS == 2) {
                                     const uint2 q = *reinterpret_cast<const uint2 *>(row);
                                     rv[0] = q.x; rv[1] = q.y;
@@ -393,24 +417,21 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                         rv[h] = q.x; rv[h + 1] = q.y; rv[h + 2] = q.z; rv[h + 3] = q.w;
                                     }
                                 }
-                                int cnt = 0, cb = 0, mis = 0;
+                                int cnt = 0, cb = 0, mt = 0;
 #pragma unroll
                                 for (int x = 0; x < W; ++x) {
                                     cnt += __popc(rv[x] & U[x]);
-                                    if (!LAB) cb += __popc(rv[x] & B[x]);
+                                    cb += __popc(rv[x] & B[0][x]);
                                 }
-                                if (LAB) { // edge label of (u, t_k) vs the g1 edge label (v_i, v_q_k)
-                                    const int u = 32 * w + __ffs(lb) - 1;
+                                if (LAB) { // edges (u, t) whose g2 label equals the g1 label of (v_i, v_q)
 #pragma unroll
-                                    for (int k = 0; k < DMAX; ++k) {
-                                        if (tl[k] == MAP_DEL) continue;
-                                        const int e = s_e2[tl[k] * n2p + u];
-                                        cb += (e != 0);
-                                        mis += (e != 0) & (e != s_pl[k]);
-                                    }
+                                    for (int l = 0; l < LMAX; ++l)
+                                        if ((lmask >> l) & 1u)
+#pragma unroll
+                                            for (int x = 0; x < W; ++x) mt += __popc(rv[W + l * W + x] & B[1 + l][x]);
                                 }
                                 // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
-                                const int x = pb + (int)rv[W] + c.eins * cnt - ee * cb + c.esub * mis;
+                                const int x = pb + (int)rv[CVW] + c.eins * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
                                 return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
@@ -441,58 +462,44 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         uint32_t U[W];
 #pragma unroll
                         for (int w = 0; w < W; ++w) U[w] = sU[w * Kc + p];
+                        uint32_t B[NB][W];
+#pragma unroll
+                        for (int b = 0; b < NB; ++b)
+#pragma unroll
+                            for (int w = 0; w < W; ++w)
+                                B[b][w] = (b == 0 || ((lmask >> (b - 1)) & 1u)) ? PBT[((int64_t)b * W + w) * Kc + p] : 0u;
                         int ped_s[W];
-                        if (!LAB) {
-                            uint32_t B[W];
 #pragma unroll
-                            for (int w = 0; w < W; ++w) B[w] = PBT[(int64_t)w * Kc + p];
+                        for (int s = 0; s < W; ++s) {
+                            const int u = lane + 32 * s;
+                            int cnt = 0, cb = 0, mt = 0;
 #pragma unroll
-                            for (int s = 0; s < W; ++s) {
-                                int cnt = 0, cb = 0;
-#pragma unroll
-                                for (int w = 0; w < W; ++w) {
-                                    const uint32_t rw = (lane + 32 * s < n2) ? sAdj[(lane + 32 * s) * W + w] : 0u;
-                                    cnt += __popc(rw & U[w]);
-                                    cb += __popc(rw & B[w]);
-                                }
-                                ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - ee * cb;
+                            for (int w = 0; w < W; ++w) {
+                                const uint32_t rw = (u < n2) ? sAdj[u * W + w] : 0u;
+                                cnt += __popc(rw & U[w]);
+                                cb += __popc(rw & B[0][w]);
                             }
-                        } else {
-                            int cb[W], mis[W];
+                            if (LAB) {
 #pragma unroll
-                            for (int s = 0; s < W; ++s) { cb[s] = 0; mis[s] = 0; }
-                            for (int k = 0; k < d; ++k) {
-                                const int tt = (k < DMAX) ? sT[k * Kc + p] : PmapT[(int64_t)s_pq[k] * Kc + p];
-                                if (tt == MAP_DEL) continue;
-                                const int ll = s_pl[k];
-                                const uint8_t *row = s_e2 + tt * n2p;
+                                for (int l = 0; l < LMAX; ++l)
+                                    if ((lmask >> l) & 1u)
 #pragma unroll
-                                for (int s = 0; s < W; ++s) {
-                                    const int u = lane + 32 * s;
-                                    const int e = (u < n2p) ? row[u] : 0;
-                                    cb[s] += (e != 0);
-                                    mis[s] += (e != 0) & (e != ll);
-                                }
+                                        for (int w = 0; w < W; ++w)
+                                            mt += __popc(((u < n2) ? sAdjL[(u * LMAX + l) * W + w] : 0u) & B[1 + l][w]);
                             }
-#pragma unroll
-                            for (int s = 0; s < W; ++s) {
-                                int cnt = 0;
-#pragma unroll
-                                for (int w = 0; w < W; ++w)
-                                    cnt += __popc(((lane + 32 * s < n2) ? sAdj[(lane + 32 * s) * W + w] : 0u) & U[w]);
-                                ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - ee * cb[s] + c.esub * mis[s];
-                            }
+                            ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - eeB * cb -
+                                       (LAB ? c.esub * mt : 0);
                         }
                         uint8_t *crow = codes + sOff[p];
                         int r = 0;
-                        const unsigned lmask = lanemask_lt();
+                        const unsigned lmk = lanemask_lt();
 #pragma unroll
                         for (int s = 0; s < W; ++s) {
                             const int u = lane + 32 * s;
                             const bool sub = (u < n2) && !((U[s] >> lane) & 1u);
                             const unsigned bal = __ballot_sync(FULL, sub);
                             const int code = sub ? rank_code(ped_s[s], base, win) : CODE_INVALID;
-                            if (sub) crow[r + __popc(bal & lmask)] = (uint8_t)code;
+                            if (sub) crow[r + __popc(bal & lmk)] = (uint8_t)code;
                             hist_add(code);
                             r += __popc(bal);
                         }
@@ -661,22 +668,20 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                     const int pedp = Pped[p];
                     if (j == n2) ped = pedp + dDel;
                     else {
-                        int cnt = 0, cb = 0, mis = 0;
+                        int cnt = 0, cb = 0, mt = 0;
 #pragma unroll
-                        for (int w = 0; w < W; ++w) cnt += __popc(sAdj[j * W + w] & Up[w]);
-                        if (!LAB) {
-#pragma unroll
-                            for (int w = 0; w < W; ++w) cb += __popc(sAdj[j * W + w] & PBT[(int64_t)w * Kc + p]);
-                        } else {
-                            for (int q = 0; q < d; ++q) {
-                                const int t = PmapT[(int64_t)s_pq[q] * Kc + p];
-                                if (t == MAP_DEL) continue;
-                                const int e = s_e2[t * n2p + j];
-                                cb += (e != 0);
-                                mis += (e != 0) & (e != s_pl[q]);
-                            }
+                        for (int w = 0; w < W; ++w) {
+                            cnt += __popc(sAdj[j * W + w] & Up[w]);
+                            cb += __popc(sAdj[j * W + w] & PBT[(int64_t)w * Kc + p]);
                         }
-                        ped = pedp + ((vl2[j] == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - ee * cb + c.esub * mis;
+                        if (LAB)
+#pragma unroll
+                            for (int l = 0; l < LMAX; ++l)
+                                if ((lmask >> l) & 1u)
+#pragma unroll
+                                    for (int w = 0; w < W; ++w)
+                                        mt += __popc(sAdjL[(j * LMAX + l) * W + w] & PBT[((int64_t)(1 + l) * W + w) * Kc + p]);
+                        ped = pedp + ((vl2[j] == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
                     }
                 }
                 Qped[k] = ped;
@@ -697,7 +702,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 for (int x = threadIdx.x; x < nk4; x += NT) {
                     const int k0 = 4 * x;
                     int pp[4];
-                    uint32_t last = 0, Bn[4][W];
+                    uint32_t last = 0, Bn[4][W]; // (unlabelled: B of the next level, built during the copy)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
                         const int k = min(k0 + b, Nn - 1);
@@ -707,7 +712,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         last |= ((j == n2) ? (uint32_t)MAP_DEL : (uint32_t)j) << (8 * b);
 #pragma unroll
                         for (int w = 0; w < W; ++w)
-                            Bn[b][w] = (inext && j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u;
+                            Bn[b][w] = (!LAB && inext && j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u;
                     }
                     // lambda columns 0..i-1: gather 8 columns x 4 survivors into registers, then store
                     // (loads of a chunk are issued together; QmapT/PmapT are distinct buffers)
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             const int q = q0 + z;
                             if (q >= i) break;
                             *reinterpret_cast<uint32_t *>(QmapT + (int64_t)q * Kc + k0) = wd[z];
-                            if ((s_pnext[q >> 5] >> (q & 31)) & 1u) { // v_q is an earlier neighbour of v_{i+1}
+                            if (!LAB && ((s_pnext[q >> 5] >> (q & 31)) & 1u)) { // v_q is an earlier neighbour of v_{i+1}
 #pragma unroll
                                 for (int b = 0; b < 4; ++b) {
                                     const uint32_t t = (wd[z] >> (8 * b)) & 0xffu;
@@ -739,10 +744,48 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         }
                     }
                     *reinterpret_cast<uint32_t *>(QmapT + (int64_t)i * Kc + k0) = last;
+                    if (i + 1 < n1) {
+                        if (!LAB) {
 #pragma unroll
-                    for (int w = 0; w < W; ++w)
+                            for (int w = 0; w < W; ++w)
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) QBT[(int64_t)w * Kc + k0 + b] = Bn[b][w];
+                                for (int b = 0; b < 4; ++b) QBT[(int64_t)w * Kc + k0 + b] = Bn[b][w];
+                        } else {
+                            // labelled: B and its label planes from the (few) columns of P_{i+1}, after the copy
+                            uint32_t Bl[4][NB][W];
+#pragma unroll
+                            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                                for (int pl2 = 0; pl2 < NB; ++pl2)
+#pragma unroll
+                                    for (int w = 0; w < W; ++w) Bl[b][pl2][w] = 0u;
+                            for (int e = 0; e < dn; ++e) {
+                                const int q = s_pnq[e], ql = s_pnl[q];
+                                uint32_t wv = last; // column i: the survivors' own targets
+                                if (q < i) {
+                                    const uint8_t *row = QmapT + (int64_t)q * Kc; // (this thread wrote it above)
+                                    wv = *reinterpret_cast<const uint32_t *>(row + k0);
+                                }
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    const uint32_t t = (wv >> (8 * b)) & 0xffu;
+#pragma unroll
+                                    for (int w = 0; w < W; ++w) {
+                                        const uint32_t bt = (t != (uint32_t)MAP_DEL && (int)(t >> 5) == w) ? (1u << (t & 31)) : 0u;
+                                        Bl[b][0][w] |= bt;
+#pragma unroll
+                                        for (int pl2 = 1; pl2 < NB; ++pl2) Bl[b][pl2][w] |= (ql == pl2) ? bt : 0u;
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int pl2 = 0; pl2 < NB; ++pl2)
+#pragma unroll
+                                for (int w = 0; w < W; ++w)
+#pragma unroll
+                                    for (int b = 0; b < 4; ++b) QBT[((int64_t)pl2 * W + w) * Kc + k0 + b] = Bl[b][pl2][w];
+                        }
+                    }
                 }
             }
             children += ci;
@@ -762,6 +805,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
         {
             const int32_t *Pped = fped(cur);
             const uint32_t *PusedT = fused(cur);
+            unsigned long long mykey = ~0ull;
             for (int k = threadIdx.x; k < N; k += NT) {
                 uint32_t U[W];
                 int usedc = 0, e2u2 = 0;
@@ -775,13 +819,17 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         bits &= bits - 1;
                         const int u = 32 * w + b;
 #pragma unroll
-                        for (int x = 0; x < W; ++x) e2u2 += __popc(__ldg(adj2 + u * W + x) & U[x]);
+                        for (int x = 0; x < W; ++x) e2u2 += __popc(sAdj[u * W + x] & U[x]);
                     }
                 }
                 const int64_t total = (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) +
                                       (int64_t)c.eins * (pd.m2 - e2u2 / 2);
-                atomicMin(&s_best, ((unsigned long long)total << 32) | (unsigned)k);
+                mykey = min(mykey, ((unsigned long long)total << 32) | (unsigned)k);
             }
+            // argmin by (total, position): warp minimum, then one shared atomic per warp
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mykey = min(mykey, __shfl_xor_sync(FULL, mykey, o));
+            if (lane == 0 && mykey != ~0ull) atomicMin(&s_best, mykey);
             block_sync();
             const unsigned long long best = s_best;
             const int kb = (int)(best & 0xffffffffull);

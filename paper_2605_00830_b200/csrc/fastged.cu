@@ -215,24 +215,34 @@ int64_t frontier_cap(int n1, int n2, int64_t k) {
 }
 
 // Per-CTA bytes of the batched kernel's per-level work arrays (the layout run_batch plans), in 64 bits.
-size_t batched_work_bytes(int64_t Kc, int W, int csmax, bool lab) {
+size_t batched_work_bytes(int64_t Kc, int W, int csmax) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
-    return a16(4 * (size_t)Kc * W) + a16(4 * (size_t)(Kc + 1)) + (lab ? a16((size_t)fg::DMAX * Kc) : 0) +
-           a16((size_t)Kc * csmax) + a16(4 * (size_t)Kc) + a16(2 * ((size_t)Kc * csmax / 16 + 2));
+    return a16(4 * (size_t)Kc * W) + a16(4 * (size_t)(Kc + 1)) + a16((size_t)Kc * csmax) + a16(4 * (size_t)Kc) +
+           a16(2 * ((size_t)Kc * csmax / 16 + 2));
 }
 
-// Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024 (P_{i+1} membership bitmask),
-// and every 32-bit offset of the plan fits: the codes of one level (Kc * csmax bytes, indexed with
-// int32 in the kernel) and the work arrays stay below 2^31 with room to spare.  csmax is taken at the
-// top of the pair's word-width bucket (the group's plan uses the bucket maximum).  Pairs beyond the
-// limits are solved by the whole-GPU kernel (solve_large), inside a batch as well.
-bool fits_batched(int n1, int n2, int64_t k) {
-    if (n2 > 128 || n1 > 1024) return false;
+// Batched-path limits: n2 <= 128 (lane-owned rows, W <= 4), n1 <= 1024, at most fg::LMAX distinct g2
+// edge labels (label planes), and every 32-bit offset of the plan fits: the codes of one level
+// (Kc * csmax bytes, indexed with int32 in the kernel), the work arrays and the frontier rows stay
+// below 2^31 with room to spare.  csmax is taken at the top of the pair's word-width bucket (the
+// group's plan uses the bucket maximum).  Pairs beyond the limits are solved by the whole-GPU kernel
+// (solve_large), inside a batch as well.
+bool fits_batched(int n1, int n2, int64_t k, int nlab) {
+    if (n2 > 128 || n1 > 1024 || nlab > fg::LMAX) return false;
     const int W = words_for(n2);
     const int64_t Kc = (frontier_cap(n1, n2, k) + 3) & ~3ll;
     const int csmax = (32 * W + 1 + 3) & ~3;
     const int64_t lim = ((int64_t)1 << 31) - ((int64_t)1 << 24);
-    return Kc * csmax < lim && (int64_t)batched_work_bytes(Kc, W, csmax, true) < lim;
+    const int64_t n1s = std::max(4, (n1 + 3) & ~3);
+    return Kc * csmax < lim && (int64_t)batched_work_bytes(Kc, W, csmax) < lim && Kc * n1s < lim;
+}
+
+// Number of distinct g2 edge labels (the label planes of a labelled pair).
+int g2_label_count(const fastged_graph_t *g2) {
+    std::vector<int32_t> l(g2->elabels ? g2->elabels : nullptr, g2->elabels ? g2->elabels + g2->m : nullptr);
+    if (!g2->elabels) return g2->m > 0 ? 1 : 0;
+    std::sort(l.begin(), l.end());
+    return (int)(std::unique(l.begin(), l.end()) - l.begin());
 }
 
 // ---------------------------------------------------------------- packing
@@ -274,6 +284,7 @@ void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, i
         return q;
     };
     d.n1 = n1; d.n2 = n2; d.m1 = g1->m; d.m2 = g2->m; d.labelled = lab ? 1 : 0; d.n2p = n2p;
+    d.nlab = 0; d.pad0 = 0;
     int32_t *vl1 = (int32_t *)seg(4 * (size_t)n1, d.vl1);
     int32_t *vl2 = (int32_t *)seg(4 * (size_t)n2, d.vl2);
     int32_t *pptr = (int32_t *)seg(4 * (size_t)(n1 + 1), d.pptr);
@@ -299,6 +310,7 @@ void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, i
             }
         }
         memset(e2, 0, (size_t)n2p * n2p);
+        d.nlab = (int)ids.size();
     }
     // P_i = {q < i : (v_q, v_i) in E1}, each g1 edge listed at its later endpoint (second-endpoint rule, C7)
     std::vector<int> cnt(n1 + 1, 0);
@@ -520,7 +532,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
                         ((int64_t)d.m1 + d.m2) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
         if (bound >= ((int64_t)1 << 31))
             fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
-        if (fits_batched(d.n1, d.n2, k) && !(h->flags & FASTGED_FLAG_FORCE_LARGE))
+        if (fits_batched(d.n1, d.n2, k, d.labelled ? d.nlab : 0) && !(h->flags & FASTGED_FLAG_FORCE_LARGE))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
             b->large.push_back(p); // solved by the whole-GPU kernel after the batched launches
@@ -581,32 +593,33 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.n1max = std::max(4, (n1max + 3) & ~3);
         a.csmax = (n2max + 1 + 3) & ~3;
         const size_t Kc = (size_t)a.Kc;
-        const int n2p = (n2max + 3) & ~3;
+        const int NB = key.lab ? 1 + fg::LMAX : 1;
         // always-shared small arrays
         size_t sm = 0;
-        a.sm.pq = (int)sm; sm += align16(4 * (size_t)a.n1max);
-        a.sm.pl = (int)sm; sm += align16(4 * (size_t)a.n1max);
-        a.sm.e2 = (int)sm; sm += key.lab ? align16((size_t)n2p * n2p) : 0;
-        a.sm.adj = (int)sm; sm += align16(4 * (size_t)std::max(n2max, 1) * W);
-        a.sm.adjh = (int)sm; sm += align16(4 * (size_t)32 * W * fg::hrow_stride(W));
+        auto sput = [&](int32_t &field, size_t bytes) { field = (int)sm; sm += align16(bytes); };
+        sput(a.sm.pq, 4 * (size_t)a.n1max);
+        sput(a.sm.pl, 4 * (size_t)a.n1max);
+        sput(a.sm.pnl, (size_t)a.n1max);
+        sput(a.sm.pnq, 4 * (size_t)a.n1max);
+        sput(a.sm.adj, 4 * (size_t)std::max(n2max, 1) * W);
+        sput(a.sm.adjl, key.lab ? 4 * (size_t)std::max(n2max, 1) * fg::LMAX * W : 0);
+        sput(a.sm.adjh, 4 * (size_t)32 * W * fg::hrow_stride(W, key.lab));
         // per-level work arrays
         size_t wk = 0;
         auto put = [&](int32_t &field, size_t bytes) { field = (int)wk; wk += align16(bytes); };
-        a.sm.ped = 0;                      // (unused: survivor PEDs go straight to the next frontier)
         put(a.sm.u, 4 * Kc * W);           // parent used masks
         put(a.sm.b, 4 * (Kc + 1));         // compact code offsets
-        put(a.sm.t, key.lab ? (size_t)fg::DMAX * Kc : 0);
-        put(a.sm.codes, Kc * a.csmax);
-        put(a.sm.sel, 4 * Kc);
-        put(a.sm.pidx, 2 * (Kc * a.csmax / 16 + 2));
+        put(a.sm.codes, Kc * a.csmax);     // rank codes of the level
+        put(a.sm.sel, 4 * Kc);             // survivors
+        put(a.sm.pidx, 2 * (Kc * a.csmax / 16 + 2)); // code position -> parent index
         const bool in_smem = sm + wk + 8192 <= h->smem_optin;
         size_t smem = sm;
         if (in_smem) {
-            for (int32_t *f : {&a.sm.u, &a.sm.b, &a.sm.t, &a.sm.codes, &a.sm.sel, &a.sm.pidx}) *f += (int)sm;
+            for (int32_t *f : {&a.sm.u, &a.sm.b, &a.sm.codes, &a.sm.sel, &a.sm.pidx}) *f += (int)sm;
             smem += wk;
         }
         a.sm.bytes = (int)smem;
-        size_t per_cta = 2 * Kc * (4 + 8 * (size_t)W + a.n1max) + (in_smem ? 0 : wk);
+        size_t per_cta = 2 * Kc * (4 + 4 * (size_t)W + 4 * (size_t)W * NB + (size_t)a.n1max) + (in_smem ? 0 : wk);
         per_cta = (per_cta + 255) & ~(size_t)255;
         void *kern = batch_kernel_for(W, key.lab, in_smem);
         if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);
@@ -1221,7 +1234,8 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
             solve_sharded(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }
-        if (!fits_batched(g1->n, g2->n, k) || (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
+        if (!fits_batched(g1->n, g2->n, k, labelled_pair(g1, g2) ? g2_label_count(g2) : 0) ||
+            (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }
