@@ -39,6 +39,9 @@
 
 namespace fg {
 
+#ifndef FG_CZ
+#define FG_CZ 4 // children evaluated per iteration of the wide branch loop (independent chains)
+#endif
 #ifndef FG_MINBLOCKS
 #define FG_MINBLOCKS 2 // resident CTAs per SM requested from ptxas (A/B experiments)
 #endif
@@ -436,19 +439,21 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             };
                             uint32_t F = Vm[w] & ~U[w];
                             while (F) { // four free targets per iteration (independent chains); lb = 0: no child
-                                uint32_t lz[4];
+                                uint32_t lz[FG_CZ];
 #pragma unroll
-                                for (int z = 0; z < 4; ++z) { lz[z] = F & (0u - F); F ^= lz[z]; }
-                                int cz[4];
+                                for (int z = 0; z < FG_CZ; ++z) { lz[z] = F & (0u - F); F ^= lz[z]; }
+                                int cz[FG_CZ];
 #pragma unroll
-                                for (int z = 0; z < 4; ++z) cz[z] = child_code(lz[z]);
+                                for (int z = 0; z < FG_CZ; ++z) cz[z] = child_code(lz[z]);
 #pragma unroll
-                                for (int z = 0; z < 4; ++z)
+                                for (int z = 0; z < FG_CZ; ++z)
                                     if (z == 0 || lz[z]) {
                                         crow[r + z] = (uint8_t)cz[z];
                                         atomicAdd(&whist[cz[z]], 1); // codes 0 and win+1 land in unused bins
                                     }
-                                r += 1 + (lz[1] != 0u) + (lz[2] != 0u) + (lz[3] != 0u);
+                                r += 1;
+#pragma unroll
+                                for (int z = 1; z < FG_CZ; ++z) r += (lz[z] != 0u);
                             }
                         }
                         const int cdel = rank_code(pedp + dDel, base, win); // deletion child (C5)
@@ -571,6 +576,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 auto valid = [](uint32_t x) { const uint32_t y = ~x; return (((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y) & 0x80808080u; };
                 int lt = 0, eq = 0;
                 unsigned long long cmask = 0ull; // words of the run holding a code <= t (runs of <= 64 words)
+#pragma unroll 4
                 for (int x = w0; x < w1; ++x) {
                     const uint32_t v = cw[x];
                     if (keepall) lt += __popc(valid(v));
@@ -612,10 +618,11 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                 eq_seen += ne;
                             }
                         }
-                        while (m) {
-                            sel[out++] = (uint32_t)(4 * x + ((__ffs(m) - 1) >> 3));
-                            m &= m - 1;
-                        }
+                        // up to four survivors of the word, written without a bit loop (no chain between them)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if ((m >> (8 * b + 7)) & 1u) sel[out + __popc(m & ((1u << (8 * b)) - 1u))] = (uint32_t)(4 * x + b);
+                        out += __popc(m);
                     }
                 }
                 if (threadIdx.x == 0) {
@@ -634,8 +641,17 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
             // flat code position -> (p, child j); PED from the code (recomputed for a saturated code);
             // the survivor's PED and used mask go straight to the next frontier (coalesced over k)
             int pmin = 0x7fffffff;
-            for (int k = threadIdx.x; k < Nn; k += NT) {
-                const int idx = (int)sel[k];
+            for (int kb = threadIdx.x; kb < Nn; kb += 4 * NT) {
+            // the positions of up to four survivors are read first, so their decode chains overlap
+            // (the in-place sel[] writes below would otherwise order every load after the previous store)
+            int idxv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) idxv[u] = (kb + u * NT < Nn) ? (int)sel[kb + u * NT] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = kb + u * NT;
+                if (k >= Nn) break;
+                const int idx = idxv[u];
                 int p;
                 if (Kc <= 65535) { // owner of position 16 (idx / 16), advanced to the owner of idx
                     p = sPidx[idx >> 4];
@@ -690,6 +706,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                     QusedT[(int64_t)w * Kc + k] = Up[w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
                 pmin = min(pmin, ped);
             }
+            }
             pmin = __reduce_min_sync(FULL, (unsigned)pmin); // PEDs are >= 0: unsigned min = signed min
             if (lane == 0 && pmin != 0x7fffffff) atomicMin(&s_lo, pmin);
             block_sync(); // the (p, j) of every survivor is in sel
@@ -716,8 +733,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                     }
                     // lambda columns 0..i-1: gather 8 columns x 4 survivors into registers, then store
                     // (loads of a chunk are issued together; QmapT/PmapT are distinct buffers)
-                    for (int q0 = 0; q0 < i; q0 += 8) {
-                        uint32_t wd[8];
+                    // (software-pipelined: the gathers of chunk c + 1 are issued before the stores of chunk c)
+                    auto gather8 = [&](int q0, uint32_t (&wd)[8]) {
 #pragma unroll
                         for (int z = 0; z < 8; ++z) {
                             const int q = min(q0 + z, i - 1);
@@ -727,6 +744,14 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             wd[z] = (uint32_t)row[pp[0]] | ((uint32_t)row[pp[1]] << 8) |
                                     ((uint32_t)row[pp[2]] << 16) | ((uint32_t)row[pp[3]] << 24);
                         }
+                    };
+                    uint32_t wnext[8];
+                    if (i > 0) gather8(0, wnext);
+                    for (int q0 = 0; q0 < i; q0 += 8) {
+                        uint32_t wd[8];
+#pragma unroll
+                        for (int z = 0; z < 8; ++z) wd[z] = wnext[z];
+                        if (q0 + 8 < i) gather8(q0 + 8, wnext);
 #pragma unroll
                         for (int z = 0; z < 8; ++z) {
                             const int q = q0 + z;
