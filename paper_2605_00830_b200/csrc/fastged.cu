@@ -770,7 +770,9 @@ void download_collect(fastged_handle_t *h, fastged_batch *b, int64_t *costs_out,
     int64_t ch = 0, pa = 0, al = 0, ops = 0;
     for (size_t p = 0; p < P; ++p) {
         ch += hch[p]; pa += hpa[p]; al += hal[p];
-        ops += hch[p] * (4 * (int64_t)b->W[p] + 8); // popcount-form lane-ops per child
+        // popcount-form lane-ops per child = 2W AND + 2W POPC + 3 cost + 2 clamp + 1
+        // histogram index (the op mix scripts/micro/int_peak.cu measures as the 'alu' peak)
+        ops += hch[p] * (4 * (int64_t)b->W[p] + 6);
     }
     h->stats.children_evaluated += ch;
     h->stats.parents_expanded += pa;

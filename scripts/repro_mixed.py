@@ -13,4 +13,8 @@ for flags in (0, binding.FLAG_DEBUG_WINDOW):
         oc, om, _ = oracle.kbest_batch([w.pair(k) for k in range(w.npairs)], w.costs, w.K)
         ok = all(gc[k] == oc[k] and np.array_equal(gm[offs[k]:offs[k+1]], om[k]) for k in range(w.npairs))
         print(w.name, flags, "parity", ok, flush=True)
+    g1, g2 = synth.large_pair(150, 0.1, seed=2)  # whole-GPU cooperative path
+    r = h.solve_pair(g1, g2, synth.COSTS["setting1"], 500)
+    o = oracle.kbest(g1, g2, synth.COSTS["setting1"], 500)
+    print("large n=150", flags, "parity", r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]), flush=True)
     h.close()
