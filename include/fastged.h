@@ -54,6 +54,11 @@ extern "C" {
 #define FASTGED_FLAG_FORCE_LARGE 4u  /* test only: solve_pair uses the whole-GPU path even for small pairs */
 #define FASTGED_FLAG_VIRTUAL_SHARDS 8u /* test only: world_size shards of one pair on this handle's GPU,
                                          exchanged by device copies instead of NCCL (rank, nccl_id ignored) */
+#define FASTGED_FLAG_LAST_BY_TOTAL 16u /* method variant: rank the last level by
+                                         PED + insertion completion instead of PED (the alternative to reading
+                                         C10 of Alg. 1); never a higher cost than the
+                                         paper-literal rule.  Batched path only (n2 <= 128): a pair that needs
+                                         the whole-GPU or sharded path fails with FASTGED_ERR_ARG. */
 
 /* Limits of this build (exceeding one returns FASTGED_ERR_CAPACITY, never a silent change). */
 #define FASTGED_MAX_N 65534        /* vertices of a source graph g1                               */

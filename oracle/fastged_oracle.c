@@ -118,11 +118,12 @@ typedef struct {
     int64_t ped;
     int64_t p; /* parent position in the frontier */
     int32_t j; /* g2 vertex index, or n2 for deletion */
+    int64_t key; /* ranking value: the PED, or (variant, last level) PED + completion */
 } cand;
 
 static int cmp_key(const void *x, const void *y) { /* (PED, p, j) ascending (C12) */
     const cand *a = (const cand *)x, *b = (const cand *)y;
-    if (a->ped != b->ped) return a->ped < b->ped ? -1 : 1;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
     if (a->p != b->p) return a->p < b->p ? -1 : 1;
     return (a->j > b->j) - (a->j < b->j);
 }
@@ -207,6 +208,8 @@ static int64_t mapping_cost(const og_graph *g1, const og_graph *g2, const og_cos
     return s;
 }
 
+#define OG_LAST_BY_TOTAL 1 /* method variant: last level ranked by PED + completion */
+
 /*
  * og_kbest: Algorithm 1 with the readings listed at the top.
  *   cost_out      : GED upper bound (the cost of the returned edit path)
@@ -215,9 +218,9 @@ static int64_t mapping_cost(const og_graph *g1, const og_graph *g2, const og_cos
  *   parents_out   : total frontier nodes expanded (sum N_i), may be NULL
  *   levels_out    : [g1->n] per-level record, may be NULL
  */
-int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t K,
-             int64_t *cost_out, int32_t *mapping_out, int64_t *children_out,
-             int64_t *parents_out, og_level *levels_out) {
+int og_kbest_ex(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t K,
+                int64_t *cost_out, int32_t *mapping_out, int64_t *children_out,
+                int64_t *parents_out, og_level *levels_out, int32_t flags) {
     int rc;
     if (!c || !cost_out || K < 1) return OG_ERR_ARG;
     if (c->vsub < 0 || c->vdel < 0 || c->vins < 0 || c->esub < 0 || c->edel < 0 || c->eins < 0)
@@ -262,6 +265,7 @@ int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t 
                 pool[slot].ped = e;
                 pool[slot].p = p;
                 pool[slot].j = j;
+                pool[slot].key = e;
             }
         }
         int64_t cnt = 0;
@@ -273,16 +277,28 @@ int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t 
 
         /* List <- best K nodes of list_tmp: the min(K, cnt) smallest keys (C12). */
         int64_t keep = cnt < K ? cnt : K;
+        if ((flags & OG_LAST_BY_TOTAL) && i == n1 - 1) {
+            /* variant: rank the last level by the total PED + completion of each child (the
+             * alternative to reading C10 of P:185-187) */
+            char *u2 = (char *)malloc((size_t)(n2 > 0 ? n2 : 1));
+            if (!u2) { free(pool); rc = OG_ERR_MEM; break; }
+            for (int64_t s = 0; s < cnt; s++) {
+                if (n2 > 0) memcpy(u2, used + pool[s].p * n2, (size_t)n2);
+                if (pool[s].j < n2) u2[pool[s].j] = 1;
+                pool[s].key = pool[s].ped + completion_cost(g2, c, u2);
+            }
+            free(u2);
+        }
         select_k(pool, cnt, keep);
         if (levels_out) {
             int64_t mn = -1, mx = -1;
             for (int64_t s = 0; s < cnt; s++)
-                if (mn < 0 || pool[s].ped < mn) mn = pool[s].ped;
+                if (mn < 0 || pool[s].key < mn) mn = pool[s].key;
             for (int64_t s = 0; s < keep; s++)
-                if (pool[s].ped > mx) mx = pool[s].ped;
+                if (pool[s].key > mx) mx = pool[s].key;
             levels_out[i].frontier = N;
             levels_out[i].candidates = cnt;
-            levels_out[i].threshold = (cnt > K) ? mx : -1; /* PED of the K-th smallest key */
+            levels_out[i].threshold = (cnt > K) ? mx : -1; /* ranking value of the K-th smallest key */
             levels_out[i].min_ped = mn;
         }
         /* Next frontier in canonical (p, j) order (C13). */
@@ -325,10 +341,16 @@ int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t 
     return rc;
 }
 
+int og_kbest(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t K,
+             int64_t *cost_out, int32_t *mapping_out, int64_t *children_out,
+             int64_t *parents_out, og_level *levels_out) {
+    return og_kbest_ex(g1, g2, c, K, cost_out, mapping_out, children_out, parents_out, levels_out, 0);
+}
+
 /* Independent pairs in parallel (no change to any pair's arithmetic). */
-int og_kbest_batch(int32_t npairs, const og_graph *g1s, const og_graph *g2s, const og_costs *c,
-                   int64_t K, int64_t *costs_out, int32_t *mappings_out, const int64_t *map_offsets,
-                   int64_t *children_out, int32_t nthreads, int32_t *status_out) {
+int og_kbest_batch_ex(int32_t npairs, const og_graph *g1s, const og_graph *g2s, const og_costs *c,
+                      int64_t K, int64_t *costs_out, int32_t *mappings_out, const int64_t *map_offsets,
+                      int64_t *children_out, int32_t nthreads, int32_t *status_out, int32_t flags) {
     if (npairs < 0 || (npairs > 0 && (!g1s || !g2s || !costs_out || !map_offsets || !status_out)))
         return OG_ERR_ARG;
 #ifdef _OPENMP
@@ -338,13 +360,20 @@ int og_kbest_batch(int32_t npairs, const og_graph *g1s, const og_graph *g2s, con
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t k = 0; k < npairs; k++) {
         int64_t ch = 0;
-        status_out[k] = og_kbest(&g1s[k], &g2s[k], c, K, &costs_out[k],
-                                 mappings_out ? mappings_out + map_offsets[k] : NULL, &ch, NULL, NULL);
+        status_out[k] = og_kbest_ex(&g1s[k], &g2s[k], c, K, &costs_out[k],
+                                    mappings_out ? mappings_out + map_offsets[k] : NULL, &ch, NULL, NULL, flags);
         if (children_out) children_out[k] = ch;
     }
     for (int32_t k = 0; k < npairs; k++)
         if (status_out[k] != OG_OK) { rc = status_out[k]; break; }
     return rc;
+}
+
+int og_kbest_batch(int32_t npairs, const og_graph *g1s, const og_graph *g2s, const og_costs *c,
+                   int64_t K, int64_t *costs_out, int32_t *mappings_out, const int64_t *map_offsets,
+                   int64_t *children_out, int32_t nthreads, int32_t *status_out) {
+    return og_kbest_batch_ex(npairs, g1s, g2s, c, K, costs_out, mappings_out, map_offsets, children_out, nthreads,
+                             status_out, 0);
 }
 
 int og_max_threads(void) {
@@ -362,7 +391,7 @@ int og_select(const int64_t *ped, const int64_t *p, const int32_t *j, int64_t n,
     cand *a = (cand *)malloc(sizeof(cand) * (size_t)(n > 0 ? n : 1));
     char *take = (char *)calloc((size_t)(n > 0 ? n : 1), 1);
     if (!a || !take) { free(a); free(take); return OG_ERR_MEM; }
-    for (int64_t x = 0; x < n; x++) { a[x].ped = ped[x]; a[x].p = p[x]; a[x].j = j[x]; }
+    for (int64_t x = 0; x < n; x++) { a[x].ped = ped[x]; a[x].key = ped[x]; a[x].p = p[x]; a[x].j = j[x]; }
     int64_t keep = k < n ? k : n;
     select_k(a, n, keep);
     /* map each selected key back to its input index (keys are unique) */

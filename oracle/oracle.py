@@ -66,6 +66,10 @@ def lib():
         L.og_kbest_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(OgCosts), C.c_int64,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
         L.og_kbest_batch.restype = C.c_int
+        L.og_kbest_ex.argtypes = L.og_kbest.argtypes + [C.c_int32]
+        L.og_kbest_ex.restype = C.c_int
+        L.og_kbest_batch_ex.argtypes = L.og_kbest_batch.argtypes + [C.c_int32]
+        L.og_kbest_batch_ex.restype = C.c_int
         L.og_mapping_cost.argtypes = [C.POINTER(OgGraph), C.POINTER(OgGraph), C.POINTER(OgCosts),
                                       C.c_void_p, C.POINTER(C.c_int64)]
         L.og_mapping_cost.restype = C.c_int
@@ -93,15 +97,19 @@ def _costs(c):
     return OgCosts(*[int(x) for x in c])
 
 
-def kbest(g1, g2, costs, K, levels: bool = False):
+LAST_BY_TOTAL = 1  # method variant: last level ranked by PED + completion
+
+
+def kbest(g1, g2, costs, K, levels: bool = False, flags: int = 0):
     """Returns dict(cost, mapping, children, parents[, levels])."""
     keep = []
     G1, G2 = _graph(g1, keep), _graph(g2, keep)
     cost, ch, pa = C.c_int64(0), C.c_int64(0), C.c_int64(0)
     mp = np.zeros(max(int(g1.n), 1), np.int32)
     lv = (OgLevel * max(int(g1.n), 1))() if levels else None
-    rc = lib().og_kbest(C.byref(G1), C.byref(G2), C.byref(_costs(costs)), int(K), C.byref(cost),
-                        mp.ctypes.data, C.byref(ch), C.byref(pa), C.cast(lv, C.c_void_p) if levels else None)
+    rc = lib().og_kbest_ex(C.byref(G1), C.byref(G2), C.byref(_costs(costs)), int(K), C.byref(cost),
+                           mp.ctypes.data, C.byref(ch), C.byref(pa), C.cast(lv, C.c_void_p) if levels else None,
+                           int(flags))
     if rc != 0:
         raise OracleError(rc)
     out = dict(cost=int(cost.value), mapping=mp[: int(g1.n)].copy(), children=int(ch.value), parents=int(pa.value))
@@ -111,7 +119,7 @@ def kbest(g1, g2, costs, K, levels: bool = False):
     return out
 
 
-def kbest_batch(pairs, costs, K, nthreads: int = 0):
+def kbest_batch(pairs, costs, K, nthreads: int = 0, flags: int = 0):
     """pairs: sequence of (g1, g2).  Returns (costs int64[P], mappings list, children int64[P])."""
     keep = []
     P = len(pairs)
@@ -126,9 +134,9 @@ def kbest_batch(pairs, costs, K, nthreads: int = 0):
     out_ch = np.zeros(max(P, 1), np.int64)
     out_m = np.zeros(max(int(offs[-1]), 1), np.int32)
     st = np.zeros(max(P, 1), np.int32)
-    rc = lib().og_kbest_batch(P, C.cast(G1, C.c_void_p), C.cast(G2, C.c_void_p), C.byref(_costs(costs)), int(K),
-                              out_c.ctypes.data, out_m.ctypes.data, offs.ctypes.data, out_ch.ctypes.data,
-                              int(nthreads), st.ctypes.data)
+    rc = lib().og_kbest_batch_ex(P, C.cast(G1, C.c_void_p), C.cast(G2, C.c_void_p), C.byref(_costs(costs)), int(K),
+                                 out_c.ctypes.data, out_m.ctypes.data, offs.ctypes.data, out_ch.ctypes.data,
+                                 int(nthreads), st.ctypes.data, int(flags))
     if rc != 0:
         raise OracleError(rc)
     maps = [out_m[offs[k]:offs[k + 1]].copy() for k in range(P)]

@@ -20,6 +20,7 @@ FLAG_TIMING = 1
 FLAG_DEBUG_WINDOW = 2
 FLAG_FORCE_LARGE = 4
 FLAG_VIRTUAL_SHARDS = 8
+FLAG_LAST_BY_TOTAL = 16  # method variant: last level ranked by PED + completion (batched path only)
 
 # The symbols include/fastged.h declares (checked by tests/test_abi.py).
 EXPORTS = (

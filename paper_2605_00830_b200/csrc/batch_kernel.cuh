@@ -95,6 +95,8 @@ struct BatchArgs {
     int64_t *parents_out;
     int64_t *algbytes_out;  // per pair: algorithmic frontier bytes of the search
     int64_t *levels_out;    // NULL, or [3 * n1] for a single-pair launch
+    int32_t last_by_total;  // method variant (reading C10 alternative): the last level is
+                            // ranked by PED + completion instead of PED
 };
 
 #ifdef FG_PROF
@@ -181,6 +183,25 @@ __device__ __forceinline__ void block_scan2(int a, int b, int &apre, int &bpre, 
     bpre = wb + ib - b;
     atot = ta;
     btot = tb;
+}
+
+// Insertion completion (C6) of a node whose used set is U: vins per unused g2 vertex +
+// eins per g2 edge with an unused endpoint.  Rows from shared memory.
+template <int W>
+__device__ __forceinline__ int completion_of(const uint32_t (&U)[W], const uint32_t *sAdj, int n2, int m2, const Costs &c) {
+    int usedc = 0, e2u2 = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        usedc += __popc(U[w]);
+        uint32_t bits = U[w];
+        while (bits) {
+            const int u = 32 * w + __ffs(bits) - 1;
+            bits &= bits - 1;
+#pragma unroll
+            for (int x = 0; x < W; ++x) e2u2 += __popc(sAdj[u * W + x] & U[x]);
+        }
+    }
+    return c.vins * (n2 - usedc) + c.eins * (m2 - e2u2 / 2);
 }
 
 template <int W, bool LAB, int NT, bool SMEM>
@@ -336,6 +357,9 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                 if (u < n2) sAdjH[(32 * s + (int)db_slot(1u << lane)) * HRS + CVW] = (l2 != vl1i) ? (uint32_t)c.vsub : 0u;
             }
             const int edd = c.edel * d, ee = c.edel + c.eins, dDel = c.vdel + edd;
+            // method variant: the last level ranked by total = PED + completion (children's completions
+            // differ from the parent's by vins for the used target and eins per edge to a used vertex)
+            const bool lastTot = a.last_by_total && i == n1 - 1;
             // labelled: PED = ... - (ee - esub) cB - esub * (label matches); unlabelled: - ee cB
             const int eeB = LAB ? ee - c.esub : ee;
             // P_i list, zeroed histograms, P_{i+1} membership and cv words: visible to A through the
@@ -402,7 +426,9 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             for (int w = 0; w < W; ++w)
                                 B[b][w] = (b == 0 || ((lmask >> (b - 1)) & 1u)) ? PBT[((int64_t)b * W + w) * Kc + p] : 0u;
                         uint8_t *crow = codes + sOff[p];
-                        const int pb = pedp - base + 1 + edd;
+                        const int comp = lastTot ? completion_of<W>(U, sAdj, n2, pd.m2, c) : 0; // parent's completion
+                        const int pb = pedp - base + 1 + edd + (lastTot ? comp - c.vins : 0);
+                        const int einsT = lastTot ? 0 : c.eins; // (total: the eins cnt of the child cancels)
                         int r = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
@@ -434,7 +460,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                             for (int x = 0; x < W; ++x) mt += __popc(rv[W + l * W + x] & B[1 + l][x]);
                                 }
                                 // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
-                                const int x = pb + (int)rv[CVW] + c.eins * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
+                                const int x = pb + (int)rv[CVW] + einsT * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
                                 return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
@@ -456,7 +482,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                 for (int z = 1; z < FG_CZ; ++z) r += (lz[z] != 0u);
                             }
                         }
-                        const int cdel = rank_code(pedp + dDel, base, win); // deletion child (C5)
+                        const int cdel = rank_code(pedp + dDel + comp, base, win); // deletion child (C5)
                         crow[r] = (uint8_t)cdel;
                         hist_add(cdel);
                     }
@@ -474,6 +500,20 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             for (int w = 0; w < W; ++w)
                                 B[b][w] = (b == 0 || ((lmask >> (b - 1)) & 1u)) ? PBT[((int64_t)b * W + w) * Kc + p] : 0u;
                         int ped_s[W];
+                        int comp = 0; // (variant) the parent's completion
+                        if (lastTot) {
+                            int e2u2 = 0, usedc = 0;
+#pragma unroll
+                            for (int s = 0; s < W; ++s) {
+                                const int u = lane + 32 * s;
+                                usedc += __popc(U[s]);
+                                if (u < n2 && ((U[s] >> lane) & 1u))
+#pragma unroll
+                                    for (int w = 0; w < W; ++w) e2u2 += __popc(sAdj[u * W + w] & U[w]);
+                            }
+                            e2u2 = __reduce_add_sync(FULL, e2u2);
+                            comp = c.vins * (n2 - usedc) + c.eins * (pd.m2 - e2u2 / 2);
+                        }
 #pragma unroll
                         for (int s = 0; s < W; ++s) {
                             const int u = lane + 32 * s;
@@ -492,8 +532,8 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                         for (int w = 0; w < W; ++w)
                                             mt += __popc(((u < n2) ? sAdjL[(u * LMAX + l) * W + w] : 0u) & B[1 + l][w]);
                             }
-                            ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + c.eins * cnt - eeB * cb -
-                                       (LAB ? c.esub * mt : 0);
+                            ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + (lastTot ? 0 : c.eins * cnt) - eeB * cb -
+                                       (LAB ? c.esub * mt : 0) + (lastTot ? comp - c.vins : 0);
                         }
                         uint8_t *crow = codes + sOff[p];
                         int r = 0;
@@ -509,7 +549,7 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                             r += __popc(bal);
                         }
                         if (lane == 0) {
-                            const int cdel = rank_code(pedp + dDel, base, win);
+                            const int cdel = rank_code(pedp + dDel + comp, base, win);
                             crow[r] = (uint8_t)cdel;
                             hist_add(cdel);
                         }
@@ -699,8 +739,14 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                                         mt += __popc(sAdjL[(j * LMAX + l) * W + w] & PBT[((int64_t)(1 + l) * W + w) * Kc + p]);
                         ped = pedp + ((vl2[j] == vl1i) ? 0 : c.vsub) + edd + c.eins * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
                     }
+                    if (lastTot) { // variant: the code stands for the total; recompute the child's completion
+                        uint32_t Uc[W];
+#pragma unroll
+                        for (int w = 0; w < W; ++w) Uc[w] = Up[w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
+                        ped += completion_of<W>(Uc, sAdj, n2, pd.m2, c);
+                    }
                 }
-                Qped[k] = ped;
+                Qped[k] = ped; // (variant, last level: the total)
 #pragma unroll
                 for (int w = 0; w < W; ++w)
                     QusedT[(int64_t)w * Kc + k] = Up[w] | ((j < n2 && (j >> 5) == w) ? (1u << (j & 31)) : 0u);
@@ -847,8 +893,10 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS) kbest_batch_kernel(const Bat
                         for (int x = 0; x < W; ++x) e2u2 += __popc(sAdj[u * W + x] & U[x]);
                     }
                 }
-                const int64_t total = (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) +
-                                      (int64_t)c.eins * (pd.m2 - e2u2 / 2);
+                // (variant: the last level already stored PED + completion; n1 = 0 has no last level)
+                const int64_t total = (a.last_by_total && n1 > 0)
+                                          ? (int64_t)Pped[k]
+                                          : (int64_t)Pped[k] + (int64_t)c.vins * (n2 - usedc) + (int64_t)c.eins * (pd.m2 - e2u2 / 2);
                 mykey = min(mykey, ((unsigned long long)total << 32) | (unsigned)k);
             }
             // argmin by (total, position): warp minimum, then one shared atomic per warp

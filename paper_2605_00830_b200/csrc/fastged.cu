@@ -636,6 +636,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.parents_out = (int64_t *)b->dpar.p;
         a.algbytes_out = (int64_t *)b->dalg.p;
         a.levels_out = levels_dev;
+        a.last_by_total = (h->flags & FASTGED_FLAG_LAST_BY_TOTAL) ? 1 : 0;
         const fg::PairDesc &d0 = b->descs[order_all[start]]; // (the group's largest pair: sorted above)
         plans.push_back(GroupLaunch{a, kern, grid, smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
         gi++;
@@ -806,6 +807,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
                  const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
                  const LargeDst *dst) {
     const int n1 = g1->n, n2 = g2->n;
+    if (h->flags & FASTGED_FLAG_LAST_BY_TOTAL)
+        fail(FASTGED_ERR_ARG, "FASTGED_FLAG_LAST_BY_TOTAL is implemented on the batched path only (n2 <= 128)");
     if (n2 > FASTGED_MAX_N2) fail(FASTGED_ERR_CAPACITY, "target graph has n2=%d > %d (limit of this build)", n2, FASTGED_MAX_N2);
     const int64_t Kc64 = frontier_cap(n1, n2, k);
     if (Kc64 > (int64_t)1 << 30) fail(FASTGED_ERR_CAPACITY, "frontier cap %lld too large", (long long)Kc64);

@@ -210,6 +210,35 @@ def test_per_level_trace(fg, oracle, flags):
     h.close()
 
 
+# ------------------------------------------------------------------ method variant (NEXT-4)
+@pytest.mark.parametrize("window", [0, 2], ids=["window127", "window2"])
+def test_variant_last_by_total_matches_oracle(fg, oracle, window):
+    """FASTGED_FLAG_LAST_BY_TOTAL (last level ranked by PED + completion, the alternative to reading C10)
+    against the oracle's variant, bit-exact, on ER, labelled molecule and n1 != n2 pairs; the whole-GPU
+    path refuses the flag."""
+    flags = fg.FLAG_LAST_BY_TOTAL | (fg.FLAG_DEBUG_WINDOW if window else 0)
+    h = fg.Handle(0, flags=flags)
+    w3 = synth.config_workload(3, npairs=50, K=300)
+    w2 = synth.config_workload(2, npairs=200)
+    rng = synth.rng_for(61)
+    odd = [(synth.er_graph(rng, int(rng.integers(2, 30)), 0.3, 3), synth.er_graph(rng, int(rng.integers(2, 60)), 0.2, 3))
+           for _ in range(30)]
+    for pairs, costs, K in (([w3.pair(k) for k in range(w3.npairs)], w3.costs, w3.K),
+                            ([w2.pair(k) for k in range(w2.npairs)], w2.costs, w2.K),
+                            (odd, COSTS["setting2"], 40)):
+        gc, gm, gch = gpu_batch(fg, h, pairs, costs, K)
+        oc, om, och = oracle.kbest_batch(pairs, costs, K, flags=oracle.LAST_BY_TOTAL)
+        lc, _, _ = oracle.kbest_batch(pairs, costs, K)
+        for k in range(len(pairs)):
+            assert gc[k] == oc[k] and np.array_equal(gm[k], om[k]) and gch[k] == och[k], k
+            assert gc[k] <= lc[k]
+    g1, g2 = synth.large_pair(150, 0.1, seed=3)
+    with pytest.raises(fg.FastGedError) as e:
+        h.solve_pair(g1, g2, COSTS["setting1"], 100)
+    assert e.value.code == fg.ERR_ARG
+    h.close()
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_cases(fg, handle, oracle):
     rng = synth.rng_for(31)

@@ -104,6 +104,34 @@ def test_hand_traces_k2(oracle_lib, case):
     assert int(bruteforce.costs_of(g1, g2, case["costs"], r["mapping"][None, :])[0]) == r["cost"]
 
 
+@pytest.mark.parametrize("case", _k2_cases(), ids=lambda c: c["name"])
+def test_variant_last_by_total_hand_traces(oracle_lib, case):
+    """NEXT-4 variant (last level ranked by PED + completion): the hand-traced values."""
+    g1, g2 = _g(case["g1"]), _g(case["g2"])
+    r = oracle_lib.kbest(g1, g2, case["costs"], case["K"], flags=oracle_lib.LAST_BY_TOTAL)
+    assert r["cost"] == case["variant_cost"] and r["mapping"].tolist() == case["variant_mapping"]
+
+
+def test_variant_never_worse_and_exact_at_full_width(oracle_lib):
+    """The variant keeps the same frontier up to the last level and then the K smallest totals, so its
+    cost is <= the paper-literal cost for every K, >= the exact GED, and = exact once K covers the widths."""
+    from oracle import bruteforce
+    rng = synth.rng_for(4040)
+    for k in range(150):
+        n1, n2 = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        g1 = synth.er_graph(rng, n1, (0.2, 0.5, 0.8)[k % 3], 2, 1 + k % 2)
+        g2 = synth.er_graph(rng, n2, (0.2, 0.5, 0.8)[k % 3], 2, 1 + k % 2)
+        c = (COSTS["unit"], COSTS["setting1"], ASYM)[k % 3]
+        ged = bruteforce.exact_ged(g1, g2, c)[0]
+        for K in (1, 2, 5, bruteforce.width(n1, n2, n1)):
+            lit = oracle_lib.kbest(g1, g2, c, K)["cost"]
+            var = oracle_lib.kbest(g1, g2, c, K, flags=oracle_lib.LAST_BY_TOTAL)
+            assert ged <= var["cost"] <= lit
+            assert oracle_lib.mapping_cost(g1, g2, c, var["mapping"]) == var["cost"]
+            if K >= bruteforce.width(n1, n2, n1):
+                assert var["cost"] == ged
+
+
 def test_selection_examples(oracle_lib):
     """P5: the selection step keeps the k smallest unique keys."""
     sel = oracle_lib.select
