@@ -384,6 +384,143 @@ int og_max_threads(void) {
 #endif
 }
 
+/* ------------------------------------------------------------------------------------------------
+ * Exact GED by depth-first branch and bound: the same
+ * vertex-branching tree as og_kbest (v_0..v_{n1-1}; children = substitutions by ascending g2 index,
+ * then the deletion), the same incremental PED (Alg. 2 P:247 with the implied edges of P:103-116) and
+ * the same completion at the leaves.  A subtree is pruned when PED + lower_bound >= the
+ * incumbent, with the admissible bound of S:275:
+ *   max(0, |R1| - |R2|) vdel + max(0, |R2| - |R1|) vins + max(0, e1 - e2) edel + max(0, e2 - e1) eins,
+ * R1 / R2 = unresolved g1 / unused g2 vertices, e1 / e2 = edges with both endpoints in R1 / R2.
+ * The incumbent starts from og_kbest at K = K0 (a pruning aid only; the optimum does not depend on it).
+ * node_limit bounds the expansions: beyond it the incumbent is returned with *optimal_out = 0.
+ * ------------------------------------------------------------------------------------------------ */
+typedef struct {
+    const og_graph *g1, *g2;
+    const og_costs *c;
+    const char *has1, *has2;
+    const int32_t *lab1, *lab2;
+    int64_t *rem1;       /* rem1[i] = g1 edges with both endpoints >= i */
+    int32_t *map;        /* current path: map[q], q < depth */
+    char *used;          /* used g2 vertices */
+    int64_t best;        /* incumbent cost */
+    int32_t *best_map;
+    int64_t nodes, limit;
+    int over;
+} bnb_state;
+
+static int64_t bnb_lower_bound(const bnb_state *S, int i, int nused, int64_t rem2) {
+    const og_costs *c = S->c;
+    const int64_t r1 = S->g1->n - i, r2 = S->g2->n - nused, e1 = S->rem1[i];
+    return (r1 > r2 ? (r1 - r2) * c->vdel : (r2 - r1) * c->vins) +
+           (e1 > rem2 ? (e1 - rem2) * c->edel : (rem2 - e1) * c->eins);
+}
+
+/* depth i: v_i is branched; ped = PED of the node; nused / e2u / rem2 = used g2 vertices, g2 edges with
+ * both endpoints used, g2 edges with both endpoints unused */
+static void bnb_dfs(bnb_state *S, int i, int64_t ped, int nused, int64_t e2u, int64_t rem2) {
+    const og_graph *g1 = S->g1, *g2 = S->g2;
+    const int n1 = g1->n, n2 = g2->n;
+    if (S->over) return;
+    if (i == n1) { /* leaf: insertion completion */
+        const int64_t total = ped + (int64_t)S->c->vins * (n2 - nused) + (int64_t)S->c->eins * (g2->m - e2u);
+        if (total < S->best) {
+            S->best = total;
+            memcpy(S->best_map, S->map, sizeof(int32_t) * (size_t)n1);
+        }
+        return;
+    }
+    if (++S->nodes > S->limit) { S->over = 1; return; }
+    for (int j = 0; j <= n2; j++) { /* substitutions ascending, then the deletion */
+        const int op = (j == n2) ? DEL : j;
+        if (op != DEL && S->used[op]) continue;
+        int64_t e = ped + vertex_cost(g1, g2, S->c, i, op);
+        for (int q = 0; q < i; q++)
+            e += edge_charge(S->has1, S->lab1, n1, S->has2, S->lab2, n2, S->c, i, op, q, S->map[q]);
+        int cu = 0, cf = 0; /* used / unused g2 neighbours of op */
+        if (op != DEL)
+            for (int u = 0; u < n2; u++)
+                if (u != op && S->has2[op * n2 + u]) { if (S->used[u]) cu++; else cf++; }
+        const int nu = nused + (op != DEL), ne2u = (int)e2u + cu;
+        const int64_t nrem2 = rem2 - cf;
+        if (e + bnb_lower_bound(S, i + 1, nu, nrem2) >= S->best) continue; /* prune */
+        S->map[i] = op;
+        if (op != DEL) S->used[op] = 1;
+        bnb_dfs(S, i + 1, e, nu, ne2u, nrem2);
+        if (op != DEL) S->used[op] = 0;
+        if (S->over) return;
+    }
+}
+
+int og_exact(const og_graph *g1, const og_graph *g2, const og_costs *c, int64_t K0, int64_t node_limit,
+             int64_t *cost_out, int32_t *mapping_out, int64_t *nodes_out, int32_t *optimal_out) {
+    int rc;
+    if (!c || !cost_out || node_limit < 1 || K0 < 1) return OG_ERR_ARG;
+    if ((rc = validate_graph(g1)) != OG_OK) return rc;
+    if ((rc = validate_graph(g2)) != OG_OK) return rc;
+    if (g1->n > 0 && !mapping_out) return OG_ERR_ARG;
+    const int n1 = g1->n, n2 = g2->n;
+    bnb_state S;
+    memset(&S, 0, sizeof S);
+    S.g1 = g1; S.g2 = g2; S.c = c; S.limit = node_limit;
+    const size_t a1 = (size_t)(n1 > 0 ? n1 * n1 : 1), a2 = (size_t)(n2 > 0 ? n2 * n2 : 1);
+    char *has1 = (char *)malloc(a1), *has2 = (char *)malloc(a2);
+    int32_t *lab1 = (int32_t *)malloc(a1 * sizeof(int32_t)), *lab2 = (int32_t *)malloc(a2 * sizeof(int32_t));
+    S.rem1 = (int64_t *)calloc((size_t)n1 + 1, sizeof(int64_t));
+    S.map = (int32_t *)calloc((size_t)(n1 > 0 ? n1 : 1), sizeof(int32_t));
+    S.best_map = (int32_t *)calloc((size_t)(n1 > 0 ? n1 : 1), sizeof(int32_t));
+    S.used = (char *)calloc((size_t)(n2 > 0 ? n2 : 1), 1);
+    rc = OG_OK;
+    if (!has1 || !has2 || !lab1 || !lab2 || !S.rem1 || !S.map || !S.best_map || !S.used) rc = OG_ERR_MEM;
+    else if (dense_adjacency(g1, has1, lab1) != OG_OK || dense_adjacency(g2, has2, lab2) != OG_OK) rc = OG_ERR_INPUT;
+    if (rc == OG_OK) {
+        S.has1 = has1; S.has2 = has2; S.lab1 = lab1; S.lab2 = lab2;
+        for (int e = 0; e < g1->m; e++) { /* rem1[i] = edges with both endpoints >= i */
+            int lo = g1->edges[2 * e] < g1->edges[2 * e + 1] ? g1->edges[2 * e] : g1->edges[2 * e + 1];
+            for (int i = 0; i <= lo; i++) S.rem1[i]++;
+        }
+        /* incumbent: the K-Best result at K0 (S: "incumbent initialized by the K=1 greedy result") */
+        int64_t kc = 0;
+        rc = og_kbest(g1, g2, c, K0, &kc, S.best_map, NULL, NULL, NULL);
+        if (rc == OG_OK) {
+            if (n1 > 0) memcpy(mapping_out, S.best_map, sizeof(int32_t) * (size_t)n1);
+            /* best = kc + 1 so that the strict prune (PED + LB >= best) keeps every path of cost <= kc:
+             * the K-Best path itself is never pruned (its prefixes satisfy PED + LB <= kc) */
+            S.best = kc + 1;
+            bnb_dfs(&S, 0, 0, 0, 0, g2->m);
+            if (S.best <= kc) { /* a leaf of cost <= kc was reached */
+                *cost_out = S.best;
+                if (n1 > 0) memcpy(mapping_out, S.best_map, sizeof(int32_t) * (size_t)n1);
+            } else
+                *cost_out = kc; /* (only when the budget ran out before any leaf) */
+            if (nodes_out) *nodes_out = S.nodes;
+            if (optimal_out) *optimal_out = !S.over;
+            if (mapping_cost(g1, g2, c, has1, has2, lab2, mapping_out) != *cost_out) rc = OG_ERR_SELFCHECK;
+        }
+    }
+    free(has1); free(has2); free(lab1); free(lab2); free(S.rem1); free(S.map); free(S.best_map); free(S.used);
+    return rc;
+}
+
+/* Pairs in parallel (independent searches). */
+int og_exact_batch(int32_t npairs, const og_graph *g1s, const og_graph *g2s, const og_costs *c, int64_t K0,
+                   int64_t node_limit, int64_t *costs_out, int32_t *mappings_out, const int64_t *map_offsets,
+                   int64_t *nodes_out, int32_t *optimal_out, int32_t nthreads, int32_t *status_out) {
+    if (npairs < 0 || (npairs > 0 && (!g1s || !g2s || !costs_out || !map_offsets || !status_out || !optimal_out)))
+        return OG_ERR_ARG;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t k = 0; k < npairs; k++)
+        status_out[k] = og_exact(&g1s[k], &g2s[k], c, K0, node_limit, &costs_out[k],
+                                 mappings_out ? mappings_out + map_offsets[k] : NULL, nodes_out ? &nodes_out[k] : NULL,
+                                 &optimal_out[k]);
+    for (int32_t k = 0; k < npairs; k++)
+        if (status_out[k] != OG_OK) return status_out[k];
+    return OG_OK;
+}
+
 /* Exposed for the selection pin: indices of the k smallest keys
  * (ped[x], p[x], j[x]) as chosen by select_k, ascending by index. */
 int og_select(const int64_t *ped, const int64_t *p, const int32_t *j, int64_t n, int64_t k, int64_t *idx_out) {

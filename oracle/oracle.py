@@ -66,6 +66,12 @@ def lib():
         L.og_kbest_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(OgCosts), C.c_int64,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
         L.og_kbest_batch.restype = C.c_int
+        L.og_exact.argtypes = [C.POINTER(OgGraph), C.POINTER(OgGraph), C.POINTER(OgCosts), C.c_int64, C.c_int64,
+                               C.POINTER(C.c_int64), C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.og_exact.restype = C.c_int
+        L.og_exact_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(OgCosts), C.c_int64, C.c_int64,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        L.og_exact_batch.restype = C.c_int
         L.og_kbest_ex.argtypes = L.og_kbest.argtypes + [C.c_int32]
         L.og_kbest_ex.restype = C.c_int
         L.og_kbest_batch_ex.argtypes = L.og_kbest_batch.argtypes + [C.c_int32]
@@ -141,6 +147,45 @@ def kbest_batch(pairs, costs, K, nthreads: int = 0, flags: int = 0):
         raise OracleError(rc)
     maps = [out_m[offs[k]:offs[k + 1]].copy() for k in range(P)]
     return out_c[:P].copy(), maps, out_ch[:P].copy()
+
+
+def exact(g1, g2, costs, K0: int = 1, node_limit: int = 10 ** 9):
+    """Exact GED by DFS branch and bound (SURVEY 8(f) NEXT-1).  Returns dict(cost, mapping, nodes, optimal);
+    optimal is False when node_limit expansions ran out (cost is then the best path found)."""
+    keep = []
+    G1, G2 = _graph(g1, keep), _graph(g2, keep)
+    cost, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+    mp = np.zeros(max(int(g1.n), 1), np.int32)
+    rc = lib().og_exact(C.byref(G1), C.byref(G2), C.byref(_costs(costs)), int(K0), int(node_limit), C.byref(cost),
+                        mp.ctypes.data, C.byref(nodes), C.byref(opt))
+    if rc != 0:
+        raise OracleError(rc)
+    return dict(cost=int(cost.value), mapping=mp[: int(g1.n)].copy(), nodes=int(nodes.value), optimal=bool(opt.value))
+
+
+def exact_batch(pairs, costs, K0: int = 1, node_limit: int = 10 ** 9, nthreads: int = 0):
+    """Exact GED of every pair (OpenMP over pairs).  Returns (costs, mappings, nodes, optimal)."""
+    keep = []
+    P = len(pairs)
+    G1 = (OgGraph * max(P, 1))()
+    G2 = (OgGraph * max(P, 1))()
+    offs = np.zeros(P + 1, np.int64)
+    for k, (a, b) in enumerate(pairs):
+        G1[k] = _graph(a, keep)
+        G2[k] = _graph(b, keep)
+        offs[k + 1] = offs[k] + int(a.n)
+    out_c = np.zeros(max(P, 1), np.int64)
+    out_n = np.zeros(max(P, 1), np.int64)
+    out_o = np.zeros(max(P, 1), np.int32)
+    out_m = np.zeros(max(int(offs[-1]), 1), np.int32)
+    st = np.zeros(max(P, 1), np.int32)
+    rc = lib().og_exact_batch(P, C.cast(G1, C.c_void_p), C.cast(G2, C.c_void_p), C.byref(_costs(costs)), int(K0),
+                              int(node_limit), out_c.ctypes.data, out_m.ctypes.data, offs.ctypes.data,
+                              out_n.ctypes.data, out_o.ctypes.data, int(nthreads), st.ctypes.data)
+    if rc != 0:
+        raise OracleError(rc)
+    maps = [out_m[offs[k]:offs[k + 1]].copy() for k in range(P)]
+    return out_c[:P].copy(), maps, out_n[:P].copy(), out_o[:P].astype(bool)
 
 
 def mapping_cost(g1, g2, costs, mapping) -> int:

@@ -21,17 +21,10 @@ C10_ALT = """        if (i == n1 - 1) /* MUTANT: rank the last level by PED + co
             for (int64_t s = 0; s < cnt; s++) {
                 char *u = used + pool[s].p * (int64_t)n2;
                 if (pool[s].j < n2) u[pool[s].j] = 1;
-                pool[s].ped += completion_cost(g2, c, u);
+                pool[s].key = pool[s].ped + completion_cost(g2, c, u);
                 if (pool[s].j < n2) u[pool[s].j] = 0;
             }
         select_k(pool, cnt, keep);
-        if (i == n1 - 1)
-            for (int64_t s = 0; s < cnt; s++) {
-                char *u = used + pool[s].p * (int64_t)n2;
-                if (pool[s].j < n2) u[pool[s].j] = 1;
-                pool[s].ped -= completion_cost(g2, c, u);
-                if (pool[s].j < n2) u[pool[s].j] = 0;
-            }
 """
 
 # (name, exact text in the source, replacement)
@@ -42,7 +35,7 @@ MUTANTS = [
      "    if (a->p != b->p) return a->p > b->p ? -1 : 1;\n    return (a->j > b->j) - (a->j < b->j);\n}\nstatic int cmp_pos"),
     ("C12: child tie key reversed", "    return (a->j > b->j) - (a->j < b->j);\n}\nstatic int cmp_pos",
      "    return (a->j < b->j) - (a->j > b->j);\n}\nstatic int cmp_pos"),
-    ("C12: PED order reversed", "    if (a->ped != b->ped) return a->ped < b->ped ? -1 : 1;", "    if (a->ped != b->ped) return a->ped > b->ped ? -1 : 1;"),
+    ("C12: PED order reversed", "    if (a->key != b->key) return a->key < b->key ? -1 : 1;", "    if (a->key != b->key) return a->key > b->key ? -1 : 1;"),
     ("keep K + 1 survivors", "        int64_t keep = cnt < K ? cnt : K;\n", "        int64_t keep = cnt < K + 1 ? cnt : K + 1;\n"),
     ("keep K - 1 survivors", "        int64_t keep = cnt < K ? cnt : K;\n", "        int64_t keep = cnt < K - 1 || K == 1 ? (cnt < K ? cnt : K) : K - 1;\n"),
     ("edel <-> eins in the implied-edge charge", "    if (e1) return c->edel;\n    if (e2) return c->eins;",
@@ -62,6 +55,13 @@ MUTANTS = [
     ("used target not marked in the child", "            if (op != DEL) nused[k * n2 + op] = 1;", "            (void)0;"),
     ("argmin takes the last of equal totals", "if (best < 0 || total < best_total)", "if (best < 0 || total <= best_total)"),
     ("g1 vertices branched in reverse order", "        int64_t e = ped[p] + vertex_cost(g1, g2, c, i, op);", "        int64_t e = ped[p] + vertex_cost(g1, g2, c, n1 - 1 - i, op);"),
+    # exact branch and bound (og_exact, NEXT-1)
+    ("B&B: lower bound doubled (not admissible)", "    return (r1 > r2 ? (r1 - r2) * c->vdel : (r2 - r1) * c->vins) +",
+     "    return 2 * (r1 > r2 ? (r1 - r2) * c->vdel : (r2 - r1) * c->vins) +"),
+    ("B&B: leaf completion drops the edge insertions", "        const int64_t total = ped + (int64_t)S->c->vins * (n2 - nused) + (int64_t)S->c->eins * (g2->m - e2u);",
+     "        const int64_t total = ped + (int64_t)S->c->vins * (n2 - nused);"),
+    ("B&B: used target not released after the subtree", "        if (op != DEL) S->used[op] = 0;\n        if (S->over) return;", "        if (S->over) return;"),
+    ("B&B: g2 edges among unused vertices not decremented", "        const int64_t nrem2 = rem2 - cf;", "        const int64_t nrem2 = rem2;"),
 ]
 
 
@@ -92,7 +92,8 @@ def main():
                 continue
             env = dict(os.environ, FASTGED_ORACLE_LIB=lib)
             r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                                os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                                os.path.join(ROOT, "tests", "test_oracle_pins.py"),
+                                os.path.join(ROOT, "tests", "test_exact_oracle.py")],
                                capture_output=True, text=True, env=env, cwd=ROOT, timeout=1200)
             failed = [ln for ln in r.stdout.splitlines() if ln.startswith("FAILED")]
             if r.returncode != 0:
@@ -101,11 +102,11 @@ def main():
             else:
                 lines.append(f"SURVIVED {name}")
             print(lines[-1], flush=True)
-    lines.append(f"{killed} of {len(MUTANTS)} mutants killed by tests/test_oracle_pins.py")
+    lines.append(f"{killed} of {len(MUTANTS)} mutants killed by tests/test_oracle_pins.py + tests/test_exact_oracle.py")
     print(lines[-1])
     if args.out:
         with open(args.out, "w") as f:
-            f.write("# python scripts/oracle_mutations.py (oracle/fastged_oracle.c vs tests/test_oracle_pins.py)\n")
+            f.write("# python scripts/oracle_mutations.py (oracle/fastged_oracle.c vs tests/test_oracle_pins.py + test_exact_oracle.py)\n")
             f.write("\n".join(lines) + "\n")
     return 0 if killed == len(MUTANTS) else 1
 
