@@ -175,6 +175,44 @@ def molecule_graph(rng: np.random.Generator, kind: str) -> Graph:
     return Graph(n, vl, np.array(pairs, np.int32).reshape(-1, 2), el)
 
 
+def two_class_molecules(n_per_class: int, seed: int = 13) -> Tuple[List[Graph], np.ndarray]:
+    """A synthetic two-class corpus shaped like Mutagenicity (the IAM dataset itself is
+    not available): class 0 = Mutagenicity-like molecules (``molecule_graph(.., "muta")``); class 1 = the
+    same recipe with one or two nitro groups (an N bonded to two O, bond labels 2 and 1) attached to random
+    carbons of degree < 4 -- the structural alert of mutagenic compounds.  Labels are the class of each
+    graph; graphs alternate between the classes.  A recipe of this repo, not a paper claim."""
+    r = rng_for(seed)
+    graphs, labels = [], []
+    C, O, N = 0, 2, 3  # label ids in _MUTA_V order (C, H, O, N, ...)
+    for k in range(2 * n_per_class):
+        cls = k % 2
+        g = molecule_graph(r, "muta")
+        if cls == 1:
+            vl = list(g.vlabels.tolist())
+            pairs = [tuple(e) for e in g.edges.tolist()]
+            el = list(g.elabels.tolist())
+            deg = np.zeros(g.n, np.int32)
+            for a, b in pairs:
+                deg[a] += 1; deg[b] += 1
+            for _ in range(int(r.integers(1, 3))):
+                cand = [v for v in range(len(vl)) if vl[v] == C and deg[v] < 4]
+                if not cand:
+                    break
+                a = int(cand[int(r.integers(0, len(cand)))])
+                nn = len(vl)
+                vl += [N, O, O]
+                pairs += [(a, nn), (nn, nn + 1), (nn, nn + 2)]
+                el += [1, 2, 1]
+                deg[a] += 1
+                deg = np.concatenate([deg, [3, 1, 1]]).astype(np.int32)
+            order = sorted(range(len(pairs)), key=lambda x: pairs[x])
+            g = Graph(len(vl), np.array(vl, np.int32), np.array([pairs[x] for x in order], np.int32).reshape(-1, 2),
+                      np.array([el[x] for x in order], np.int32))
+        graphs.append(g)
+        labels.append(cls)
+    return graphs, np.array(labels, np.int32)
+
+
 # ------------------------------------------------------------------- workloads
 @dataclass
 class Workload:

@@ -239,6 +239,21 @@ def test_variant_last_by_total_matches_oracle(fg, oracle, window):
     h.close()
 
 
+# ------------------------------------------------------------------ KNN_GED (NEXT-3)
+def test_knn_ged_matrix_matches_oracle(fg, handle, oracle):
+    """The test -> train GED matrix of the KNN_GED protocol (uniform costs) from one
+    batched GPU call equals the oracle's matrix element by element, so the classification is the same."""
+    from paper_2605_00830_b200 import knn
+    graphs, y = synth.two_class_molecules(15, seed=5)
+    tr, te = knn.split_70_30(len(graphs), seed=1)
+    D = knn.ged_matrix(handle, fg.PackedGraphs(graphs), te, tr, COSTS["uniform"], 1000)
+    pairs = [(graphs[a], graphs[b]) for a in te for b in tr]
+    oc, _, _ = oracle.kbest_batch(pairs, COSTS["uniform"], 1000, nthreads=NCPU)
+    assert np.array_equal(D.reshape(-1), oc)
+    acc, pred, te2, _ = knn.knn_ged(handle, graphs, y, COSTS["uniform"], K=1000, k=1, seed=1)
+    assert np.array_equal(te2, te) and np.array_equal(pred, knn.knn_predict(oc.reshape(D.shape), y[tr], 1))
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_cases(fg, handle, oracle):
     rng = synth.rng_for(31)
