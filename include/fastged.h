@@ -197,6 +197,52 @@ int fastged_nccl_unique_id(uint8_t *out);
 /* Library version string, e.g. "fastged-b200 0.1 sm_100a". */
 const char *fastged_version(void);
 
+/* ---------------------------------------------------------------------------------------------
+ * Edit paths: the step after the search.  Host functions of the library (no
+ * device needed); the mapping is any complete vertex mapping, e.g. the one fastged_solve_* returned.
+ * ------------------------------------------------------------------------------------------------- */
+#define FASTGED_OP_VSUB 1 /* a = g1 vertex, b = its g2 image */
+#define FASTGED_OP_VDEL 2 /* a = deleted g1 vertex                                                        */
+#define FASTGED_OP_VINS 3 /* b = inserted g2 vertex                                                       */
+#define FASTGED_OP_ESUB 4 /* g1 edge (a, c) -> g2 edge (b, d) */
+#define FASTGED_OP_EDEL 5 /* g1 edge (a, c) deleted                                                       */
+#define FASTGED_OP_EINS 6 /* g2 edge (b, d) inserted                                                      */
+
+typedef struct {
+    int32_t kind;       /* FASTGED_OP_*                                   */
+    int32_t a, b, c, d; /* vertex ids as above; -1 where not applicable */
+    int32_t cost;       /* cost of the operation under the cost model (0 for an equal-label substitution) */
+} fastged_edit_op_t;
+
+/* The explicit edit path of a complete vertex mapping (mapping[i] = g2 vertex or -1 = deleted): for
+ * v_0..v_{n1-1} its vertex operation followed by the implied operations on the edges to the earlier
+ * vertices (second-endpoint rule), then the vertex insertions (ascending) and the insertions of the g2
+ * edges with an unused endpoint.  The costs sum to the path cost (*cost_out), which equals
+ * the GED a solve returned with that mapping.  ops may be NULL to query the count; max_ops = capacity.
+ * Errors: FASTGED_ERR_ARG (NULL, capacity too small: *n_ops_out still holds the count),
+ * FASTGED_ERR_INPUT (invalid graph, mapping out of range or not injective). */
+int fastged_edit_path(const fastged_graph_t *g1, const fastged_graph_t *g2, const fastged_costs_t *c,
+                      const int32_t *mapping, fastged_edit_op_t *ops, int32_t max_ops, int32_t *n_ops_out,
+                      int64_t *cost_out);
+
+/* Applies the first prefix_len VERTEX operations of the path (the n1 operations on v_0..v_{n1-1}, then the
+ * insertions) with their implied edge effects (the NAS crossover of PAPER.md:714):
+ * substituted vertices take the g2 label, deleted vertices vanish with their edges, edges between two
+ * resolved (or inserted) vertices take their g2 state, unresolved g1 vertices and the edges among them or
+ * to resolved vertices stay as in g1.  prefix_len = 0 gives g1; prefix_len = n1 + #insertions gives a
+ * graph equal to g2 under origin_out.  Output vertices: the surviving g1 vertices in index order, then the
+ * inserted g2 vertices ascending.  origin_out[v] = g2 vertex of output vertex v, or -1 - (g1 index) for an
+ * unresolved g1 vertex.  Capacities: vlabels_out/origin_out [n1 + n2], edges_out [2 (m1 + m2)],
+ * elabels_out [m1 + m2].  Errors as fastged_edit_path; prefix_len out of range -> FASTGED_ERR_ARG. */
+int fastged_apply_edit_path(const fastged_graph_t *g1, const fastged_graph_t *g2, const int32_t *mapping,
+                            int32_t prefix_len, int32_t *n_out, int32_t *vlabels_out, int32_t *origin_out,
+                            int32_t *m_out, int32_t *edges_out, int32_t *elabels_out);
+
+/* 1 if a and b are equal under the bijection mapping (a vertex v -> b vertex mapping[v]): same vertex
+ * labels and the same edges with the same labels; 0 if not; negative FASTGED_ERR_* (negated) on a mapping
+ * that is not a bijection or a NULL argument. */
+int fastged_graphs_equal_under_mapping(const fastged_graph_t *a, const fastged_graph_t *b, const int32_t *mapping);
+
 #ifdef __cplusplus
 }
 #endif

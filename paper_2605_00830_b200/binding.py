@@ -27,7 +27,9 @@ EXPORTS = (
     "fastged_create", "fastged_destroy", "fastged_last_error", "fastged_solve_pair", "fastged_solve_pair_ex",
     "fastged_solve_batch", "fastged_batch_upload", "fastged_batch_run", "fastged_batch_download",
     "fastged_batch_free", "fastged_get_stats", "fastged_version", "fastged_nccl_unique_id",
+    "fastged_edit_path", "fastged_apply_edit_path", "fastged_graphs_equal_under_mapping",
 )
+OP_NAMES = {1: "vsub", 2: "vdel", 3: "vins", 4: "esub", 5: "edel", 6: "eins"}
 
 
 class FastGedError(RuntimeError):
@@ -58,6 +60,10 @@ class ConfigT(C.Structure):
 class ResultT(C.Structure):
     _fields_ = [("cost", C.c_int64), ("mapping", C.c_void_p), ("children_evaluated", C.c_int64),
                 ("parents_expanded", C.c_int64), ("device_ms", C.c_float)]
+
+
+class EditOpT(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("kind", "a", "b", "c", "d", "cost")]
 
 
 class StatsT(C.Structure):
@@ -100,6 +106,13 @@ def lib(path: Optional[str] = None):
     L.fastged_version.restype = C.c_char_p
     L.fastged_nccl_unique_id.argtypes = [P]
     L.fastged_nccl_unique_id.restype = C.c_int
+    L.fastged_edit_path.argtypes = [C.POINTER(GraphT), C.POINTER(GraphT), C.POINTER(CostsT), P, P, C.c_int32,
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+    L.fastged_apply_edit_path.argtypes = [C.POINTER(GraphT), C.POINTER(GraphT), P, C.c_int32, C.POINTER(C.c_int32),
+                                          P, P, C.POINTER(C.c_int32), P, P]
+    L.fastged_graphs_equal_under_mapping.argtypes = [C.POINTER(GraphT), C.POINTER(GraphT), P]
+    for name in ("fastged_edit_path", "fastged_apply_edit_path", "fastged_graphs_equal_under_mapping"):
+        getattr(L, name).restype = C.c_int
     for name in ("fastged_create", "fastged_solve_pair", "fastged_solve_pair_ex", "fastged_solve_batch",
                  "fastged_batch_upload", "fastged_batch_run", "fastged_batch_download", "fastged_get_stats"):
         getattr(L, name).restype = C.c_int
@@ -266,6 +279,53 @@ def nccl_unique_id() -> bytes:
     if rc != OK:
         raise FastGedError(rc, "ncclGetUniqueId failed")
     return buf.raw
+
+
+def _global_error(rc: int):
+    if rc != 0:
+        raise FastGedError(rc, (lib().fastged_last_error(None) or b"").decode())
+
+
+def edit_path(g1, g2, costs, mapping):
+    """Explicit edit path of a complete mapping (fastged_edit_path): (list of (op, a, b, c, d, cost), cost)."""
+    keep = []
+    G1, G2 = _graph_struct(g1, keep), _graph_struct(g2, keep)
+    mp = _i32(mapping).reshape(-1)
+    n, cost = C.c_int32(0), C.c_int64(0)
+    _global_error(lib().fastged_edit_path(C.byref(G1), C.byref(G2), C.byref(_costs(costs)),
+                                          mp.ctypes.data if mp.size else None, None, 0, C.byref(n), C.byref(cost)))
+    ops = (EditOpT * max(n.value, 1))()
+    _global_error(lib().fastged_edit_path(C.byref(G1), C.byref(G2), C.byref(_costs(costs)),
+                                          mp.ctypes.data if mp.size else None, C.cast(ops, C.c_void_p), n.value,
+                                          C.byref(n), C.byref(cost)))
+    return [(OP_NAMES[o.kind], o.a, o.b, o.c, o.d, o.cost) for o in ops[: n.value]], int(cost.value)
+
+
+def apply_edit_path(g1, g2, mapping, prefix_len: int):
+    """The graph after the first prefix_len vertex operations (fastged_apply_edit_path).
+    Returns (Graph, origin) with origin[v] = g2 vertex or -1 - g1 index (unresolved)."""
+    from .synth import Graph
+    keep = []
+    G1, G2 = _graph_struct(g1, keep), _graph_struct(g2, keep)
+    mp = _i32(mapping).reshape(-1)
+    cap_n, cap_m = int(g1.n) + int(g2.n) + 1, int(g1.edges.shape[0]) + int(g2.edges.shape[0]) + 1
+    vl, org = np.zeros(cap_n, np.int32), np.zeros(cap_n, np.int32)
+    e, el = np.zeros(2 * cap_m, np.int32), np.zeros(cap_m, np.int32)
+    n, m = C.c_int32(0), C.c_int32(0)
+    _global_error(lib().fastged_apply_edit_path(C.byref(G1), C.byref(G2), mp.ctypes.data if mp.size else None,
+                                                int(prefix_len), C.byref(n), vl.ctypes.data, org.ctypes.data, C.byref(m),
+                                                e.ctypes.data, el.ctypes.data))
+    return Graph(n.value, vl[: n.value], e[: 2 * m.value].reshape(-1, 2), el[: m.value]), org[: n.value]
+
+
+def graphs_equal_under_mapping(a, b, mapping) -> bool:
+    keep = []
+    A, B = _graph_struct(a, keep), _graph_struct(b, keep)
+    mp = _i32(mapping).reshape(-1)
+    r = lib().fastged_graphs_equal_under_mapping(C.byref(A), C.byref(B), mp.ctypes.data if mp.size else None)
+    if r < 0:
+        _global_error(-r)
+    return bool(r)
 
 
 def version() -> str:

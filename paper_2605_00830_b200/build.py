@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfastged.so")
 SRCS = [os.path.join(HERE, "csrc", "fastged.cu")]
 DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "large_kernel.cuh", "shard_kernels.cuh",
-                                                       "shard_host.inc")] + \
+                                                       "shard_host.inc", "editpath.inc")] + \
     [os.path.join(ROOT, "include", "fastged.h")]
 
 NVCC_FLAGS = [

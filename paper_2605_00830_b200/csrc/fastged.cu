@@ -1007,6 +1007,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
 }
 
 #include "shard_host.inc"
+#include "editpath.inc"
 
 } // namespace
 
@@ -1266,6 +1267,141 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
     } catch (const std::bad_alloc &) {
         if (b) cudaStreamSynchronize(h->stream);
         return set_err(h, FgError{FASTGED_ERR_CAPACITY, "host allocation failed"});
+    }
+}
+
+int fastged_edit_path(const fastged_graph_t *g1, const fastged_graph_t *g2, const fastged_costs_t *c,
+                      const int32_t *mapping, fastged_edit_op_t *ops, int32_t max_ops, int32_t *n_ops_out,
+                      int64_t *cost_out) {
+    g_create_error.clear();
+    try {
+        if (!n_ops_out || !cost_out) fail(FASTGED_ERR_ARG, "n_ops_out / cost_out is NULL");
+        validate_costs(c);
+        validate_graph(g1, 0, "g1");
+        validate_graph(g2, 0, "g2");
+        check_mapping(g1, g2, mapping);
+        const std::vector<fastged_edit_op_t> v = edit_ops(g1, g2, c, mapping);
+        int64_t tot = 0;
+        for (const auto &o : v) tot += o.cost;
+        *n_ops_out = (int32_t)v.size();
+        *cost_out = tot;
+        if (ops) {
+            if ((int64_t)v.size() > max_ops) fail(FASTGED_ERR_ARG, "ops capacity %d < %zu operations", max_ops, v.size());
+            std::copy(v.begin(), v.end(), ops);
+        }
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        g_create_error = e.msg;
+        return e.code;
+    } catch (...) {
+        g_create_error = "host allocation failed";
+        return FASTGED_ERR_CAPACITY;
+    }
+}
+
+int fastged_apply_edit_path(const fastged_graph_t *g1, const fastged_graph_t *g2, const int32_t *mapping,
+                            int32_t prefix_len, int32_t *n_out, int32_t *vlabels_out, int32_t *origin_out,
+                            int32_t *m_out, int32_t *edges_out, int32_t *elabels_out) {
+    g_create_error.clear();
+    try {
+        if (!n_out || !m_out || !vlabels_out || !origin_out || !edges_out || !elabels_out)
+            fail(FASTGED_ERR_ARG, "an output is NULL");
+        validate_graph(g1, 0, "g1");
+        validate_graph(g2, 0, "g2");
+        check_mapping(g1, g2, mapping);
+        const int n1 = g1->n, n2 = g2->n;
+        std::vector<char> used((size_t)std::max(n2, 1), 0);
+        for (int i = 0; i < n1; ++i)
+            if (mapping[i] >= 0) used[mapping[i]] = 1;
+        std::vector<int> ins;
+        for (int u = 0; u < n2; ++u)
+            if (!used[u]) ins.push_back(u);
+        if (prefix_len < 0 || prefix_len > n1 + (int)ins.size())
+            fail(FASTGED_ERR_ARG, "prefix_len %d outside 0..%d", prefix_len, n1 + (int)ins.size());
+        const int res = std::min(prefix_len, n1);                // v_0 .. v_{res-1} are resolved
+        const int nins = std::max(0, prefix_len - n1);           // the first nins insertions are applied
+        DenseGraph A, B;
+        A.build(g1);
+        B.build(g2);
+        std::vector<int> id1((size_t)std::max(n1, 1), -1);       // output id of g1 vertex i (or -1: deleted)
+        int n = 0;
+        for (int i = 0; i < n1; ++i) {
+            if (i < res && mapping[i] < 0) continue;
+            id1[i] = n;
+            vlabels_out[n] = i < res ? g2->vlabels[mapping[i]] : g1->vlabels[i];
+            origin_out[n] = i < res ? mapping[i] : -1 - i;
+            ++n;
+        }
+        std::vector<int> g1of((size_t)n, -1); // g1 index of output vertex v (surviving g1 vertices)
+        for (int i = 0; i < n1; ++i)
+            if (id1[i] >= 0) g1of[id1[i]] = i;
+        std::vector<int> idi(ins.size(), -1);
+        for (int x = 0; x < nins; ++x) {
+            idi[x] = n;
+            vlabels_out[n] = g2->vlabels[ins[x]];
+            origin_out[n] = ins[x];
+            ++n;
+        }
+        int m = 0;
+        auto add = [&](int a, int b, int32_t l) {
+            edges_out[2 * m] = std::min(a, b);
+            edges_out[2 * m + 1] = std::max(a, b);
+            elabels_out[m] = l;
+            ++m;
+        };
+        for (int a = 0; a < n; ++a)
+            for (int b = a + 1; b < n; ++b) {
+                const bool ra = origin_out[a] >= 0, rb = origin_out[b] >= 0;
+                if (ra && rb) { // both resolved or inserted: the g2 state
+                    const int32_t l = B.at(origin_out[a], origin_out[b]);
+                    if (l >= 0) add(a, b, l);
+                } else { // at least one unresolved g1 vertex: the g1 edge (resolved later)
+                    // g1 indices (a resolved endpoint is a g1 vertex here: insertions only follow v_{n1-1})
+                    const int qa = a < (int)g1of.size() ? g1of[a] : -1, qb = b < (int)g1of.size() ? g1of[b] : -1;
+                    if (qa >= 0 && qb >= 0) {
+                        const int32_t l = A.at(qa, qb);
+                        if (l >= 0) add(a, b, l);
+                    }
+                }
+            }
+        *n_out = n;
+        *m_out = m;
+        return FASTGED_OK;
+    } catch (const FgError &e) {
+        g_create_error = e.msg;
+        return e.code;
+    } catch (...) {
+        g_create_error = "host allocation failed";
+        return FASTGED_ERR_CAPACITY;
+    }
+}
+
+int fastged_graphs_equal_under_mapping(const fastged_graph_t *a, const fastged_graph_t *b, const int32_t *mapping) {
+    g_create_error.clear();
+    try {
+        validate_graph(a, 0, "a");
+        validate_graph(b, 0, "b");
+        if (a->n != b->n) fail(FASTGED_ERR_INPUT, "not a bijection: %d vs %d vertices", a->n, b->n);
+        if (a->n > 0 && !mapping) fail(FASTGED_ERR_ARG, "mapping is NULL");
+        std::vector<char> seen((size_t)std::max(b->n, 1), 0);
+        for (int v = 0; v < a->n; ++v) {
+            if (mapping[v] < 0 || mapping[v] >= b->n || seen[mapping[v]]) fail(FASTGED_ERR_INPUT, "mapping is not a bijection");
+            seen[mapping[v]] = 1;
+        }
+        for (int v = 0; v < a->n; ++v)
+            if (a->vlabels[v] != b->vlabels[mapping[v]]) return 0;
+        if (a->m != b->m) return 0;
+        DenseGraph B;
+        B.build(b);
+        for (int e = 0; e < a->m; ++e) {
+            const int x = mapping[a->edges[2 * e]], y = mapping[a->edges[2 * e + 1]];
+            const int32_t la = a->elabels ? a->elabels[e] : 0;
+            if (B.at(x, y) != la) return 0;
+        }
+        return 1;
+    } catch (const FgError &e) {
+        g_create_error = e.msg;
+        return -e.code;
     }
 }
 
