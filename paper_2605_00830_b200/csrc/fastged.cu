@@ -458,11 +458,17 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
 #define FG_BATCH_NT 256
 #endif
 constexpr int BATCH_NT = FG_BATCH_NT; // threads per CTA of the batched kernel (A/B: -DFG_BATCH_NT=...)
+#ifndef FG_BATCH_NT_W1
+#define FG_BATCH_NT_W1 128
+#endif
+// one-word pairs (n2 <= 32) have small work arrays: a narrower CTA puts more pairs on an SM
+constexpr int BATCH_NT_W1 = FG_BATCH_NT_W1;
+inline int batch_nt(int W) { return W == 1 ? BATCH_NT_W1 : BATCH_NT; }
 constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batches into two pipelined chunks
 
 void *batch_kernel_for(int W, bool lab, bool smem) {
 #define KV(WW, LL, SS) \
-    if (W == WW && lab == LL && smem == SS) return (void *)fg::kbest_batch_kernel<WW, LL, BATCH_NT, SS>;
+    if (W == WW && lab == LL && smem == SS) return (void *)fg::kbest_batch_kernel<WW, LL, (WW == 1 ? BATCH_NT_W1 : BATCH_NT), SS>;
     KV(1, false, true) KV(1, true, true) KV(2, false, true) KV(2, true, true)
     KV(3, false, true) KV(3, true, true) KV(4, false, true) KV(4, true, true)
     KV(1, false, false) KV(1, true, false) KV(2, false, false) KV(2, true, false)
@@ -564,7 +570,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
     }
     CK(cudaMemsetAsync(b->dwork.p, 0, 64 * sizeof(int), h->stream));
     int gi = 0;
-    struct GroupLaunch { fg::BatchArgs a; void *kern; int grid; size_t smem, per_cta; int64_t cost; };
+    struct GroupLaunch { fg::BatchArgs a; void *kern; int grid, nt; size_t smem, per_cta; int64_t cost; };
     std::vector<GroupLaunch> plans;
     for (auto &sp : spans) {
         const GroupKey key = sp.first;
@@ -625,7 +631,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BATCH_NT, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, batch_nt(W), smem));
         occ = std::max(occ, 1);
         int grid = (int)std::min<int64_t>((int64_t)cnt, (int64_t)occ * h->sms);
         a.scratch = nullptr; // set below: this group's slice of the handle's scratch
@@ -638,7 +644,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.levels_out = levels_dev;
         a.last_by_total = (h->flags & FASTGED_FLAG_LAST_BY_TOTAL) ? 1 : 0;
         const fg::PairDesc &d0 = b->descs[order_all[start]]; // (the group's largest pair: sorted above)
-        plans.push_back(GroupLaunch{a, kern, grid, smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
+        plans.push_back(GroupLaunch{a, kern, grid, batch_nt(W), smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
         gi++;
     }
     // longest pairs first across the groups too: the group holding the largest pair is launched first
@@ -694,7 +700,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             CK(cudaEventRecord(e0, st));
         }
         void *params[] = {(void *)&plans[g].a};
-        CK(cudaLaunchKernel(plans[g].kern, dim3(plans[g].grid), dim3(BATCH_NT), params, plans[g].smem, st));
+        CK(cudaLaunchKernel(plans[g].kern, dim3(plans[g].grid), dim3(plans[g].nt), params, plans[g].smem, st));
         if (e1) CK(cudaEventRecord(e1, st));
         h->stats.kernel_launches++;
         if (g > 0) {
