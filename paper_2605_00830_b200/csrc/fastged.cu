@@ -463,16 +463,27 @@ constexpr int BATCH_NT = FG_BATCH_NT; // threads per CTA of the batched kernel (
 #endif
 // one-word pairs (n2 <= 32) have small work arrays: a narrower CTA puts more pairs on an SM
 constexpr int BATCH_NT_W1 = FG_BATCH_NT_W1;
-inline int batch_nt(int W) { return W == 1 ? BATCH_NT_W1 : BATCH_NT; }
+
 constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batches into two pipelined chunks
 
-void *batch_kernel_for(int W, bool lab, bool smem) {
-#define KV(WW, LL, SS) \
-    if (W == WW && lab == LL && smem == SS) return (void *)fg::kbest_batch_kernel<WW, LL, (WW == 1 ? BATCH_NT_W1 : BATCH_NT), SS>;
-    KV(1, false, true) KV(1, true, true) KV(2, false, true) KV(2, true, true)
-    KV(3, false, true) KV(3, true, true) KV(4, false, true) KV(4, true, true)
-    KV(1, false, false) KV(1, true, false) KV(2, false, false) KV(2, true, false)
-    KV(3, false, false) KV(3, true, false) KV(4, false, false) KV(4, true, false)
+// Threads per CTA of a word-width group: one warp per pair when every level of every pair in the group
+// has at most SMALL_CHILDREN candidates (e.g. AIDS-like pairs at K = 100: up to 16 pairs in flight per SM
+// instead of 2, no cross-warp barriers), 128 for the other one-word groups, 256 otherwise.
+constexpr int64_t SMALL_CHILDREN = 4096;
+int batch_nt(int W, int64_t kcap, int n2max) {
+    if (W == 1 && kcap * (n2max + 1) <= SMALL_CHILDREN) return 32;
+    return W == 1 ? BATCH_NT_W1 : BATCH_NT;
+}
+
+void *batch_kernel_for(int W, bool lab, bool smem, int nt) {
+#define KV(WW, LL, SS, NN) \
+    if (W == WW && lab == LL && smem == SS && nt == NN) return (void *)fg::kbest_batch_kernel<WW, LL, NN, SS>;
+    KV(1, false, true, 32) KV(1, true, true, 32)
+    KV(1, false, true, BATCH_NT_W1) KV(1, true, true, BATCH_NT_W1) KV(1, false, false, BATCH_NT_W1) KV(1, true, false, BATCH_NT_W1)
+    KV(2, false, true, BATCH_NT) KV(2, true, true, BATCH_NT) KV(3, false, true, BATCH_NT) KV(3, true, true, BATCH_NT)
+    KV(4, false, true, BATCH_NT) KV(4, true, true, BATCH_NT)
+    KV(2, false, false, BATCH_NT) KV(2, true, false, BATCH_NT)
+    KV(3, false, false, BATCH_NT) KV(3, true, false, BATCH_NT) KV(4, false, false, BATCH_NT) KV(4, true, false, BATCH_NT)
 #undef KV
     return nullptr;
 }
@@ -627,11 +638,12 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.sm.bytes = (int)smem;
         size_t per_cta = 2 * Kc * (4 + 4 * (size_t)W + 4 * (size_t)W * NB + (size_t)a.n1max) + (in_smem ? 0 : wk);
         per_cta = (per_cta + 255) & ~(size_t)255;
-        void *kern = batch_kernel_for(W, key.lab, in_smem);
+        const int nt = in_smem ? batch_nt(W, kcap, n2max) : batch_nt(W, 1 << 30, n2max);
+        void *kern = batch_kernel_for(W, key.lab, in_smem, nt);
         if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, batch_nt(W), smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem));
         occ = std::max(occ, 1);
         int grid = (int)std::min<int64_t>((int64_t)cnt, (int64_t)occ * h->sms);
         a.scratch = nullptr; // set below: this group's slice of the handle's scratch
@@ -644,7 +656,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.levels_out = levels_dev;
         a.last_by_total = (h->flags & FASTGED_FLAG_LAST_BY_TOTAL) ? 1 : 0;
         const fg::PairDesc &d0 = b->descs[order_all[start]]; // (the group's largest pair: sorted above)
-        plans.push_back(GroupLaunch{a, kern, grid, batch_nt(W), smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
+        plans.push_back(GroupLaunch{a, kern, grid, nt, smem, per_cta, (int64_t)d0.n1 * (d0.n2 + 1)});
         gi++;
     }
     // longest pairs first across the groups too: the group holding the largest pair is launched first
