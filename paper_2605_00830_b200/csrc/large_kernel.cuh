@@ -45,7 +45,13 @@
 namespace fg {
 namespace cg = cooperative_groups;
 
-constexpr int LNT = 512; // threads per CTA of the large kernel (one CTA per SM)
+#ifndef FG_LBR
+#define FG_LBR 4 // rows of one B-phase step with their code loads in flight together
+#endif
+#ifndef FG_LNT
+#define FG_LNT 640
+#endif
+constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per SM)
 constexpr int LPF = 2;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
 constexpr int LMAXGRID = 256; // CTAs of the large kernel (one per SM)
 
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             int wl = 0, we = 0;
             // 32 rows per step, one per lane; only rows whose smallest code can be selected are read
             // (up to 8 of them with their loads in flight together)
-            constexpr int BR = 8;
+            constexpr int BR = FG_LBR;
             for (int k0 = p0; k0 < p1; k0 += 32) {
                 const int kl = k0 + lane;
                 const bool q = kl < p1 && (keepall || a.rowmin[kl] <= tcode);
