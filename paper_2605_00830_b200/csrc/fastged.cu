@@ -889,8 +889,16 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const bool sparse = (n2 ? 2 * g2->m / n2 : 0) <= 32;
     bool csr_in_smem = false, adjT_in_smem = false;
     int nwa = fg::LNT / 32;
+    // the kernel's static shared memory (block-wide scratch) counts against the same per-CTA limit
+    size_t static_smem = 0;
+    {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, (const void *)fg::kbest_large_kernel<uint16_t, uint16_t, true>));
+        static_smem = fa.sharedSizeBytes;
+    }
+    const size_t smem_cap = (size_t)h->smem_optin - static_smem;
     auto fits = [&](bool at, bool cr, int nw) {
-        return fg::large_smem_bytes(cs, csz, n1s, esz, nw, n1r, W, n2, nnbr, at, cr) <= (size_t)h->smem_optin;
+        return fg::large_smem_bytes(cs, csz, n1s, esz, nw, n1r, W, n2, nnbr, at, cr) <= smem_cap;
     };
     if (fits(true, true, nwa)) adjT_in_smem = csr_in_smem = true;
     else if (sparse && fits(false, true, nwa)) csr_in_smem = true;
@@ -898,7 +906,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     else if (fits(false, true, nwa)) csr_in_smem = true;
     while (nwa > 1 && !fits(adjT_in_smem, csr_in_smem, nwa)) nwa--;
     const size_t smem = fg::large_smem_bytes(cs, csz, n1s, esz, nwa, n1r, W, n2, nnbr, adjT_in_smem, csr_in_smem);
-    if (smem > (size_t)h->smem_optin) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
+    if (smem > smem_cap) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
     void *kfn = nullptr;
 #define LK(M, C, L) (void *)fg::kbest_large_kernel<M, C, L>
     if (wide) kfn = c16 ? (lab ? LK(uint16_t, uint16_t, true) : LK(uint16_t, uint16_t, false))

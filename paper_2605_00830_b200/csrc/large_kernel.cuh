@@ -52,7 +52,10 @@ namespace cg = cooperative_groups;
 #define FG_LNT 640
 #endif
 constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per SM)
-constexpr int LPF = 2;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
+#ifndef FG_LPF
+#define FG_LPF 2
+#endif
+constexpr int LPF = FG_LPF;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
 constexpr int LMAXGRID = 256; // CTAs of the large kernel (one per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
