@@ -436,6 +436,15 @@ def run_pair(args, rank, local_rank, world):
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("large_kernel_dram_bytes_per_launch")
     except Exception:
         pass
+    parity = None
+    try:  # the oracle's stored result for this corner (tests/golden, written by scripts/make_golden.py)
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_cfg4.json")))["runs"].get(str(idx))
+        if gold is not None and int(gold["K"]) == int(K):
+            parity = {"checked": 1, "mismatches": int(not (r["cost"] == gold["cost"] and r["mapping"].tolist() == gold["mapping"]
+                                                           and r["children"] == gold["children"])),
+                      "against": "tests/golden/oracle_cfg4.json (oracle cost, mapping, children)"}
+    except Exception:
+        pass
     kern_s = kern_ms / args.steps / 1e3
     ach = st["alg_bytes"] / kern_s / 1e9 if (world == 1 and kern_s > 0) else None
     roof = {"bound": "hbm", "kernel": "kbest_large_kernel (all levels of the pair in one cooperative launch)",
@@ -456,6 +465,7 @@ def run_pair(args, rank, local_rank, world):
         "e2e": {"value": args.steps / wall, "unit": "pairs/s", "h2d_bytes_per_step": st["h2d_bytes"],
                 "d2h_bytes_per_step": st["d2h_bytes"]},
         "roofline": roof,
+        "parity": {"golden": parity},
         "gpu_launches": st["kernel_launches"] * args.steps,
         "clocks": clk,
     }
