@@ -1,4 +1,7 @@
-"""Summarise gpurun_out/ evidence into profiles/ (launch list, ncu full metrics, hotspots, bench lines)."""
+"""Summarise gpurun_out/ evidence into profiles/ (launch list, ncu full metrics, hotspots, bench lines).
+
+    python scripts/make_profiles.py r2      (after scripts/gpu_round.sh)
+"""
 import collections, csv, json, math, os, shutil, subprocess, sys
 R = sys.argv[1] if len(sys.argv) > 1 else "r1"
 os.makedirs("profiles", exist_ok=True)
@@ -8,7 +11,7 @@ agg = collections.defaultdict(list)
 for r in rows[1:]:
     agg[r[ik]].append(float(r[iv].replace(",", "")))
 tot = sum(sum(v) for v in agg.values())
-lines = ["# ncu launch list of `python bench.py --steps 2 --warmup 1 --no-cpu-baseline` (gpu__time_duration.sum, --clock-control none)",
+lines = ["# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (gpu__time_duration.sum, --clock-control none)",
          "# cold-cache, serialised replay: compare SHARES, not absolutes", "share   launches  mean_us  kernel"]
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"{sum(v)/tot*100:6.2f}%  {len(v):3d}  {sum(v)/len(v)/1e3:10.1f}  {k}")
@@ -36,7 +39,17 @@ for x in recs:
 valid = [d for d in dram if d is not None]
 summary = {"source": "ncu --set full --clock-control none -k regex:kbest_batch -c 3 python scripts/prof_batch.py 10000 1000 1 (the bench workload)",
            "kernels": [x['Kernel Name'] for x in recs], "dram_bytes_per_launch": dram,
-           "bench_kernel_dram_bytes_per_launch": (sum(valid) / len(valid)) if valid else None}
+           # DRAM bytes per launch of the batched kernels, keyed by bench workload (bench.py roofline.traffic)
+           "bench_kernel_dram_bytes_per_launch": {"cfg3": (sum(valid) / len(valid)) if valid else None}}
+if os.path.exists("gpurun_out/prof_cfg5.ncu-rep"):
+    o5 = subprocess.run(["ncu", "-i", "gpurun_out/prof_cfg5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r5 = list(csv.reader(o5.splitlines())); h5 = r5[0]; u5 = r5[1]
+    vals = []
+    for row in r5[2:]:
+        i1, i2 = h5.index("dram__bytes_read.sum"), h5.index("dram__bytes_write.sum")
+        vals.append((float(row[i1]) + float(row[i2])) * scale.get(u5[i1], 1))
+    summary["bench_kernel_dram_bytes_per_launch"]["cfg5"] = sum(vals) / len(vals) if vals else None
+    summary["cfg5_source"] = "ncu --set full --clock-control none -k regex:kbest_batch -c 2 python scripts/prof_cfg5.py 20000"
 if os.path.exists("gpurun_out/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500 p=0.05 K=1e5)
     o2 = subprocess.run(["ncu", "-i", "gpurun_out/prof_large5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r2 = list(csv.reader(o2.splitlines())); h2 = r2[0]; u2 = r2[1]
@@ -45,8 +58,12 @@ if os.path.exists("gpurun_out/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500
     summary["large_kernel_dram_bytes_per_launch"] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
     summary["large_source"] = "ncu --set full --clock-control none -k regex:kbest_large -c 1 python scripts/prof_large.py 5"
 json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
-subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep '(int)2' 30 > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
-for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "bench_ref.json", "time_large.txt", "nvsmi.txt"):
+subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep 'kbest_batch_kernel<(int)2' 30 "
+               f"paper_2605_00830_b200/csrc/batch_kernel.cuh > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
+if os.path.exists("gpurun_out/prof_large5.ncu-rep"):
+    subprocess.run(f"python scripts/ncu_stalls.py gpurun_out/prof_large5.ncu-rep kbest_large 30 > profiles/{R}_ncu_large_stalls.txt", shell=True)
+for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "bench_ref.json", "time_large.txt", "nvsmi.txt",
+          "smoke.log", "pytest_gpu.log"):
     if os.path.exists(f"gpurun_out/{f}"):
         shutil.copy(f"gpurun_out/{f}", f"profiles/{R}_{f}")
 print(open(f"profiles/{R}_launches_bench.txt").read()); print(json.dumps(summary, indent=1))
