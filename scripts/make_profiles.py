@@ -4,7 +4,9 @@
 """
 import collections, csv, json, math, os, shutil, subprocess, sys
 R = sys.argv[1] if len(sys.argv) > 1 else "r1"
-os.makedirs("profiles", exist_ok=True)
+REP = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"   # where the .ncu-rep files are
+OUT = sys.argv[3] if len(sys.argv) > 3 else "profiles"     # where the summaries go
+os.makedirs(OUT, exist_ok=True)
 rows = [r for r in csv.reader(open("gpurun_out/launches.csv")) if len(r) > 10]
 hdr = rows[0]; ik = hdr.index("Kernel Name"); iv = hdr.index("Metric Value")
 agg = collections.defaultdict(list)
@@ -15,8 +17,8 @@ lines = ["# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-ba
          "# cold-cache, serialised replay: compare SHARES, not absolutes", "share   launches  mean_us  kernel"]
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"{sum(v)/tot*100:6.2f}%  {len(v):3d}  {sum(v)/len(v)/1e3:10.1f}  {k}")
-open(f"profiles/{R}_launches_bench.txt", "w").write("\n".join(lines) + "\n")
-out = subprocess.run(["ncu", "-i", "gpurun_out/prof_bench.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+open(f"{OUT}/{R}_launches_bench.txt", "w").write("\n".join(lines) + "\n")
+out = subprocess.run(["ncu", "-i", f"{REP}/prof_bench.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines())); hdr = r[0]; units = r[1]
 want = ['Kernel Name', 'gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'smsp__inst_executed.sum',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
@@ -27,7 +29,7 @@ idx = {h: i for i, h in enumerate(hdr)}
 recs = [{w: row[idx[w]] for w in want if w in idx} for row in r[2:]]
 for x in recs:
     x["units"] = {w: units[idx[w]] for w in want if w in idx}
-json.dump(recs, open(f"profiles/{R}_ncu_full_batch.json", "w"), indent=1)
+json.dump(recs, open(f"{OUT}/{R}_ncu_full_batch.json", "w"), indent=1)
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 dram = []
 for x in recs:
@@ -41,8 +43,8 @@ summary = {"source": "ncu --set full --clock-control none -k regex:kbest_batch -
            "kernels": [x['Kernel Name'] for x in recs], "dram_bytes_per_launch": dram,
            # DRAM bytes per launch of the batched kernels, keyed by bench workload (bench.py roofline.traffic)
            "bench_kernel_dram_bytes_per_launch": {"cfg3": (sum(valid) / len(valid)) if valid else None}}
-if os.path.exists("gpurun_out/prof_cfg5.ncu-rep"):
-    o5 = subprocess.run(["ncu", "-i", "gpurun_out/prof_cfg5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if os.path.exists(f"{REP}/prof_cfg5.ncu-rep"):
+    o5 = subprocess.run(["ncu", "-i", f"{REP}/prof_cfg5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r5 = list(csv.reader(o5.splitlines())); h5 = r5[0]; u5 = r5[1]
     vals = []
     for row in r5[2:]:
@@ -50,20 +52,20 @@ if os.path.exists("gpurun_out/prof_cfg5.ncu-rep"):
         vals.append((float(row[i1]) + float(row[i2])) * scale.get(u5[i1], 1))
     summary["bench_kernel_dram_bytes_per_launch"]["cfg5"] = sum(vals) / len(vals) if vals else None
     summary["cfg5_source"] = "ncu --set full --clock-control none -k regex:kbest_batch -c 2 python scripts/prof_cfg5.py 20000"
-if os.path.exists("gpurun_out/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500 p=0.05 K=1e5)
-    o2 = subprocess.run(["ncu", "-i", "gpurun_out/prof_large5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if os.path.exists(f"{REP}/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500 p=0.05 K=1e5)
+    o2 = subprocess.run(["ncu", "-i", f"{REP}/prof_large5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r2 = list(csv.reader(o2.splitlines())); h2 = r2[0]; u2 = r2[1]
     def val(k):
         i = h2.index(k); return float(r2[2][i].replace(",", "")) * scale.get(u2[i], 1)
     summary["large_kernel_dram_bytes_per_launch"] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
     summary["large_source"] = "ncu --set full --clock-control none -k regex:kbest_large -c 1 python scripts/prof_large.py 5"
-json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
-subprocess.run(f"python scripts/ncu_lines.py gpurun_out/prof_bench.ncu-rep 'kbest_batch_kernel<(int)2' 30 "
-               f"paper_2605_00830_b200/csrc/batch_kernel.cuh > profiles/{R}_ncu_source_hotspots_w2.txt", shell=True)
-if os.path.exists("gpurun_out/prof_large5.ncu-rep"):
-    subprocess.run(f"python scripts/ncu_stalls.py gpurun_out/prof_large5.ncu-rep kbest_large 30 > profiles/{R}_ncu_large_stalls.txt", shell=True)
+json.dump(summary, open(f"{OUT}/ncu_summary.json", "w"), indent=1)
+subprocess.run(f"python scripts/ncu_lines.py {REP}/prof_bench.ncu-rep 'kbest_batch_kernel<(int)2' 30 "
+               f"paper_2605_00830_b200/csrc/batch_kernel.cuh > {OUT}/{R}_ncu_source_hotspots_w2.txt", shell=True)
+if os.path.exists(f"{REP}/prof_large5.ncu-rep"):
+    subprocess.run(f"python scripts/ncu_stalls.py {REP}/prof_large5.ncu-rep kbest_large 30 > {OUT}/{R}_ncu_large_stalls.txt", shell=True)
 for f in ("bench.json", "bench_cfg5.json", "bench_cfg2.json", "bench_cfg4.json", "bench_ref.json", "time_large.txt", "nvsmi.txt",
           "smoke.log", "pytest_gpu.log"):
     if os.path.exists(f"gpurun_out/{f}"):
-        shutil.copy(f"gpurun_out/{f}", f"profiles/{R}_{f}")
-print(open(f"profiles/{R}_launches_bench.txt").read()); print(json.dumps(summary, indent=1))
+        shutil.copy(f"gpurun_out/{f}", f"{OUT}/{R}_{f}")
+print(open(f"{OUT}/{R}_launches_bench.txt").read()); print(json.dumps(summary, indent=1))
