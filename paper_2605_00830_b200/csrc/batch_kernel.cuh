@@ -453,11 +453,16 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS * 256 / NT) kbest_batch_kerne
                                     cb += __popc(rv[x] & B[0][x]);
                                 }
                                 if (LAB) { // edges (u, t) whose g2 label equals the g1 label of (v_i, v_q)
+                                    // (the per-label sets are disjoint -- t is the image of one q, the edge (u, t)
+                                    // has one label -- so one POPC of their union counts them all)
 #pragma unroll
-                                    for (int l = 0; l < LMAX; ++l)
-                                        if ((lmask >> l) & 1u)
+                                    for (int x = 0; x < W; ++x) {
+                                        uint32_t mw = 0u;
 #pragma unroll
-                                            for (int x = 0; x < W; ++x) mt += __popc(rv[W + l * W + x] & B[1 + l][x]);
+                                        for (int l = 0; l < LMAX; ++l)
+                                            if ((lmask >> l) & 1u) mw |= rv[W + l * W + x] & B[1 + l][x];
+                                        mt += __popc(mw);
+                                    }
                                 }
                                 // rank code = clamp(PED - base + 1, 0, win + 1), with pb = PED_p - base + 1 + edel d_i
                                 const int x = pb + (int)rv[CVW] + einsT * cnt - eeB * cb - (LAB ? c.esub * mt : 0);
@@ -524,13 +529,15 @@ __global__ void __launch_bounds__(NT, FG_MINBLOCKS * 256 / NT) kbest_batch_kerne
                                 cnt += __popc(rw & U[w]);
                                 cb += __popc(rw & B[0][w]);
                             }
-                            if (LAB) {
+                            if (LAB) { // (disjoint per-label sets: one POPC of their union)
 #pragma unroll
-                                for (int l = 0; l < LMAX; ++l)
-                                    if ((lmask >> l) & 1u)
+                                for (int w = 0; w < W; ++w) {
+                                    uint32_t mw = 0u;
 #pragma unroll
-                                        for (int w = 0; w < W; ++w)
-                                            mt += __popc(((u < n2) ? sAdjL[(u * LMAX + l) * W + w] : 0u) & B[1 + l][w]);
+                                    for (int l = 0; l < LMAX; ++l)
+                                        if ((lmask >> l) & 1u) mw |= ((u < n2) ? sAdjL[(u * LMAX + l) * W + w] : 0u) & B[1 + l][w];
+                                    mt += __popc(mw);
+                                }
                             }
                             ped_s[s] = pedp + (int)((Mm[s] >> lane) & 1u) * c.vsub + edd + (lastTot ? 0 : c.eins * cnt) - eeB * cb -
                                        (LAB ? c.esub * mt : 0) + (lastTot ? comp - c.vins : 0);
