@@ -187,12 +187,35 @@ void validate_graph(const fastged_graph_t *g, int pair, const char *which) {
     if (g->m > 0 && !g->edges) fail(FASTGED_ERR_ARG, "pair %d: %s edges is NULL", pair, which);
     if ((int64_t)g->m > (int64_t)g->n * (g->n - 1) / 2)
         fail(FASTGED_ERR_INPUT, "pair %d: %s has more edges than a simple graph allows", pair, which);
-    std::vector<uint64_t> keys((size_t)g->m);
     for (int e = 0; e < g->m; ++e) {
         int a = g->edges[2 * e], b = g->edges[2 * e + 1];
         if (a < 0 || b < 0 || a >= g->n || b >= g->n)
             fail(FASTGED_ERR_INPUT, "pair %d: %s edge %d endpoint out of range", pair, which, e);
         if (a == b) fail(FASTGED_ERR_INPUT, "pair %d: %s edge %d is a self-loop", pair, which, e);
+    }
+    if (g->n <= 4096) { // duplicate edges: a per-thread adjacency bitmap, O(m) (host packing is on the e2e path)
+        thread_local std::vector<uint64_t> bits;
+        const size_t nw = ((size_t)g->n * g->n + 63) / 64;
+        if (bits.size() < nw) bits.assign(nw, 0);
+        bool dup = false;
+        int e = 0;
+        for (; e < g->m; ++e) {
+            const int a = std::min(g->edges[2 * e], g->edges[2 * e + 1]), b = std::max(g->edges[2 * e], g->edges[2 * e + 1]);
+            const size_t x = (size_t)a * g->n + b;
+            if ((bits[x >> 6] >> (x & 63)) & 1u) { dup = true; break; }
+            bits[x >> 6] |= 1ull << (x & 63);
+        }
+        for (int f = 0; f < e + (dup ? 1 : 0) && f < g->m; ++f) { // clear exactly the bits set above
+            const int a = std::min(g->edges[2 * f], g->edges[2 * f + 1]), b = std::max(g->edges[2 * f], g->edges[2 * f + 1]);
+            const size_t x = (size_t)a * g->n + b;
+            bits[x >> 6] &= ~(1ull << (x & 63));
+        }
+        if (dup) fail(FASTGED_ERR_INPUT, "pair %d: %s has a duplicate edge", pair, which);
+        return;
+    }
+    std::vector<uint64_t> keys((size_t)g->m);
+    for (int e = 0; e < g->m; ++e) {
+        const int a = g->edges[2 * e], b = g->edges[2 * e + 1];
         keys[e] = ((uint64_t)std::min(a, b) << 32) | (uint32_t)std::max(a, b);
     }
     std::sort(keys.begin(), keys.end());
@@ -306,28 +329,36 @@ void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, i
     else d.e2lab = 0;
     if (n1) memcpy(vl1, g1->vlabels, 4 * (size_t)n1);
     if (n2) memcpy(vl2, g2->vlabels, 4 * (size_t)n2);
-    // g2 label ids: 1..L (0 = no edge); g1 labels absent from g2 -> 255 (never equal)
-    std::map<int32_t, int> ids;
+    // g2 label ids: 1..L (0 = no edge); g1 labels absent from g2 -> 255 (never equal).  A small linear table
+    // (molecules have a handful of bond labels); per-thread scratch, no allocation per pair.
+    thread_local std::vector<std::pair<int32_t, int>> ids;
+    ids.clear();
+    auto label_id = [&](int32_t l) -> int {
+        for (const auto &x : ids)
+            if (x.first == l) return x.second;
+        return -1;
+    };
     if (lab) {
         for (int e = 0; e < g2->m; ++e) {
             int32_t l = g2->elabels ? g2->elabels[e] : 0;
-            if (!ids.count(l)) {
+            if (label_id(l) < 0) {
                 int id = (int)ids.size() + 1;
                 if (id > FASTGED_MAX_EDGE_LABELS)
                     fail(FASTGED_ERR_CAPACITY, "pair %d: g2 has more than %d distinct edge labels", pair,
                          FASTGED_MAX_EDGE_LABELS);
-                ids[l] = id;
+                ids.push_back({l, id});
             }
         }
         memset(e2, 0, (size_t)n2p * n2p);
         d.nlab = (int)ids.size();
     }
     // P_i = {q < i : (v_q, v_i) in E1}, each g1 edge listed at its later endpoint (second-endpoint rule, C7)
-    std::vector<int> cnt(n1 + 1, 0);
+    thread_local std::vector<int> cnt, fillp;
+    cnt.assign((size_t)n1 + 1, 0);
     for (int e = 0; e < g1->m; ++e) cnt[std::max(g1->edges[2 * e], g1->edges[2 * e + 1])]++;
     pptr[0] = 0;
     for (int i = 0; i < n1; ++i) pptr[i + 1] = pptr[i] + cnt[i];
-    std::vector<int> fillp(pptr, pptr + n1 + 1);
+    fillp.assign(pptr, pptr + n1 + 1);
     for (int e = 0; e < g1->m; ++e) {
         int a = g1->edges[2 * e], b = g1->edges[2 * e + 1];
         int q = std::min(a, b), i = std::max(a, b);
@@ -335,8 +366,8 @@ void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, i
         pq[at] = q;
         int32_t l = g1->elabels ? g1->elabels[e] : 0;
         if (lab) {
-            auto it = ids.find(l);
-            pl[at] = it == ids.end() ? 255 : it->second;
+            const int id = label_id(l);
+            pl[at] = id < 0 ? 255 : id;
         } else pl[at] = 0;
     }
     memset(adj2, 0, 4 * (size_t)n2 * W);
@@ -346,7 +377,7 @@ void pack_pair(const fastged_graph_t *g1, const fastged_graph_t *g2, bool lab, i
         adj2[y * W + (x >> 5)] |= 1u << (x & 31);
         if (lab) {
             int32_t l = g2->elabels ? g2->elabels[e] : 0;
-            uint8_t id = (uint8_t)ids[l];
+            uint8_t id = (uint8_t)label_id(l);
             e2[x * n2p + y] = id;
             e2[y * n2p + x] = id;
         }
