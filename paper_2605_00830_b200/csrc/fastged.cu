@@ -6,6 +6,7 @@
 // kernels, copy results back once.  Nothing of the search runs on the host.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h> // header-only NVTX v3: named host ranges for Nsight timelines
 
 #include <algorithm>
 #include <chrono>
@@ -102,6 +103,14 @@ struct FgError {
     } while (0)
 
 inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// NVTX range for the lifetime of a scope (pack / plan+launch / large pair / download / sharded level)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 inline int words_for(int n2) { return std::max(1, (n2 + 31) / 32); }
 
 // ---------------------------------------------------------------- packed pair (host side)
@@ -408,6 +417,7 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
                            const fastged_graph_t *g2s, fastged_batch *reuse = nullptr, int32_t pair_base = 0) {
     if (npairs < 0) fail(FASTGED_ERR_ARG, "npairs < 0");
     if (npairs > 0 && (!g1s || !g2s)) fail(FASTGED_ERR_ARG, "graph arrays are NULL");
+    NvtxRange nv("fastged: validate + pack + H2D");
     fastged_batch *b = reuse ? reuse : new fastged_batch();
     b->ran = false;
     b->plan_valid = false; // (its device buffers may be reallocated below)
@@ -582,6 +592,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
                int64_t *levels_dev, bool first = true) {
     validate_costs(c);
     if (k < 1) fail(FASTGED_ERR_ARG, "k < 1");
+    NvtxRange nv("fastged: plan + launch batch");
     // The launch plan of a batch (groups, scheduling order, kernel variants, grids, scratch slices) depends
     // only on (K, costs, flags) and the handle's scratch: repeated runs of a resident batch reuse it, so a
     // small batch is not dominated by host-side planning (the device sits idle while the host plans).
@@ -821,6 +832,7 @@ void finish_timing(fastged_handle_t *h) {
 // Enqueue the D2H copies of a batch's results into its staging (no sync).
 void download_enqueue(fastged_handle_t *h, fastged_batch *b) {
     if (!b->ran) fail(FASTGED_ERR_ARG, "batch was not run");
+    NvtxRange nv("fastged: D2H results");
     const size_t P = (size_t)b->npairs, M = (size_t)b->total_map;
     uint8_t *st = (uint8_t *)b->stage.p + b->res_at;
     int64_t *hc = (int64_t *)st, *hch = hc + P, *hpa = hch + P, *hal = hpa + P;
@@ -883,6 +895,7 @@ void begin_call(fastged_handle_t *h) {
 void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
                  const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
                  const LargeDst *dst) {
+    NvtxRange nv("fastged: whole-GPU pair");
     const int n1 = g1->n, n2 = g2->n;
     if (h->flags & FASTGED_FLAG_LAST_BY_TOTAL)
         fail(FASTGED_ERR_ARG, "FASTGED_FLAG_LAST_BY_TOTAL is implemented on the batched path only (n2 <= 128)");

@@ -254,6 +254,18 @@ def test_knn_ged_matrix_matches_oracle(fg, handle, oracle):
     assert np.array_equal(te2, te) and np.array_equal(pred, knn.knn_predict(oc.reshape(D.shape), y[tr], 1))
 
 
+def test_allpairs_checkpointed_matches_one_batch(fg, handle, tmp_path):
+    """The checkpointed all-pairs driver (chunks written atomically, resumed after an interruption) gives
+    the same costs and mappings as one fastged_solve_batch over all pairs."""
+    from paper_2605_00830_b200 import allpairs
+    w = synth.config_workload(5)
+    graphs = w.graphs[:30]  # 435 unordered pairs
+    assert allpairs.all_pairs(handle, graphs, w.costs, 200, str(tmp_path), chunk=100, keep_mappings=True, max_chunks=2) is None
+    ia, ib, cost, ch, maps, offs = allpairs.all_pairs(handle, graphs, w.costs, 200, str(tmp_path), chunk=100, keep_mappings=True)
+    c2, m2, o2, ch2 = handle.solve_batch(fg.PackedGraphs(graphs), ia, ib, w.costs, 200)
+    assert np.array_equal(cost, c2) and np.array_equal(ch, ch2) and np.array_equal(maps.astype(np.int32), m2)
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_cases(fg, handle, oracle):
     rng = synth.rng_for(31)
