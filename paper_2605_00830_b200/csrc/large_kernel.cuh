@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                     __syncwarp();
                     const int pb = pedp - base + 1 + edd;
+                    const int cdel = rank_code(pedp + pedDel, base, win);
                     uint8_t *crow = a.codes + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
                     CntT *qc = Qcnt + (int64_t)k * cs;
@@ -452,16 +453,13 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int u = u0 + b;
-                            int code;
-                            if (u < n2 && !((ub >> b) & 1u)) {
-                                const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
-                                              (LAB ? c.esub * ms[b] : 0);
-                                code = min(max(x, 0), win + 1);
-                            } else if (u == n2) {
-                                code = rank_code(pedp + pedDel, base, win); // deletion child (reading C5)
-                            } else {
-                                code = CODE_INVALID;
-                            }
+                            // branch-free: every slot's value is computed, then the deletion slot and the
+                            // used / out-of-range slots are selected in
+                            const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
+                                          (LAB ? c.esub * ms[b] : 0);
+                            int code = min(max(x, 0), win + 1);
+                            code = (u == n2) ? cdel : code; // deletion child (reading C5)
+                            code = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : code;
                             if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
                             word |= (uint32_t)code << (8 * b);
                             rmin = min(rmin, (uint32_t)code);
