@@ -54,7 +54,13 @@ def parse():
 
 
 def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    rank, local_rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    # test hook (tests/test_bench_multirank.py): FASTGED_BENCH_SHARE_GPU=1 puts every rank on cuda:0 with the
+    # gloo backend, so the N > 1 code path (sharding, gather, max over ranks) runs on a one-GPU box; the
+    # numbers of such a run are not a measurement of N GPUs
+    if os.environ.get("FASTGED_BENCH_SHARE_GPU") == "1":
+        local_rank = 0
+    return rank, local_rank, world
 
 
 WORKLOADS = {
@@ -278,11 +284,12 @@ def run_ours(args, rank, local_rank, world):
         assert mine_ok, "gathered results differ from the device-resident run"
 
     # ---- max over ranks
-    vals = torch.tensor([dev_ms, max(e2e_t) * len(e2e_t), wall], dtype=torch.float64, device=dev)
+    red = "cpu" if os.environ.get("FASTGED_BENCH_SHARE_GPU") == "1" else dev  # (gloo reduces host tensors)
+    vals = torch.tensor([dev_ms, max(e2e_t) * len(e2e_t), wall], dtype=torch.float64, device=red)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     dev_ms_max, e2e_max, wall_max = (float(x) for x in vals.tolist())
-    tot = torch.tensor([children, parents, alg_bytes, alg_ops], dtype=torch.float64, device=dev)
+    tot = torch.tensor([children, parents, alg_bytes, alg_ops], dtype=torch.float64, device=red)
     if world > 1:
         dist.all_reduce(tot)
     pairs_total = w.npairs * args.steps
@@ -419,7 +426,8 @@ def run_pair(args, rank, local_rank, world):
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - wall
     clk = clocks.stop()
-    vals = torch.tensor([dev_ms, wall], dtype=torch.float64, device=dev)
+    red = "cpu" if os.environ.get("FASTGED_BENCH_SHARE_GPU") == "1" else dev
+    vals = torch.tensor([dev_ms, wall], dtype=torch.float64, device=red)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     dev_ms, wall = (float(x) for x in vals.tolist())
@@ -542,7 +550,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("FASTGED_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_pair(args, rank, local_rank, world) if args.workload == "cfg4" else run_ours(args, rank, local_rank, world)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -187,6 +187,9 @@ __device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, 
     return pedp + cv + c.edel * d + c.eins * cnt - (c.edel + c.eins) * cb + c.esub * mis;
 }
 
+#ifdef FG_LSTAT
+__device__ unsigned long long fg_lstat[2];
+#endif
 template <typename MapT, typename CntT, bool LAB>
 __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
@@ -660,6 +663,15 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                 }
                 unsigned hm = __ballot_sync(FULL, has);
+#ifdef FG_LSTAT
+                {
+                    const unsigned rows = __ballot_sync(FULL, kl < N);
+                    if (lane == 0) {
+                        atomicAdd(&fg_lstat[0], (unsigned long long)__popc(hm));
+                        atomicAdd(&fg_lstat[1], (unsigned long long)__popc(rows));
+                    }
+                }
+#endif
                 int zn = hm ? __ffs(hm) - 1 : 0;
                 uint4 vn = (hm && lane < vpr) ? rowvec(kb + zn * GW, lane) : inv;
                 while (hm) {
@@ -781,6 +793,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         block_sync();
         grid.sync();
         if (blockIdx.x == 0 && threadIdx.x == 31) a.out[9] = nhist;
+#ifdef FG_LSTAT
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            printf("LSTAT parents with a survivor %llu of %llu (%.3f)\n", fg_lstat[0], fg_lstat[1], (double)fg_lstat[0] / fg_lstat[1]);
+#endif
         if (blockIdx.x == 0) {
             const unsigned long long best = *a.best;
             const int kb = (int)(best & 0xffffffffull);

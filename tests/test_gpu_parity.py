@@ -266,6 +266,23 @@ def test_allpairs_checkpointed_matches_one_batch(fg, handle, tmp_path):
     assert np.array_equal(cost, c2) and np.array_equal(ch, ch2) and np.array_equal(maps.astype(np.int32), m2)
 
 
+def test_random_torture(fg, handle, oracle):
+    """Random sizes (n1, n2 in 0..90: every word width, n1 != n2), densities, vertex-label counts, 1..5 edge
+    labels (more than 3 routes a pair to the whole-GPU path inside the batch), random costs including zeros
+    and K from 1 to 5000 -- one batch per K against the oracle, element by element."""
+    rng = synth.rng_for(9090)
+    for K in (1, 2, 3, 7, 50, 500, 5000):
+        pairs = []
+        for k in range(40):
+            nmax = 90 if K <= 500 else 40
+            n1, n2 = int(rng.integers(0, nmax)), int(rng.integers(0, nmax))
+            p = float(rng.random())
+            nv, ne = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+            pairs.append((synth.er_graph(rng, n1, p, nv, ne), synth.er_graph(rng, n2, p, nv, ne)))
+        costs = tuple(int(x) for x in rng.integers(0, 7, size=6))
+        assert_batch_parity(fg, handle, oracle, pairs, costs, K, f"torture K={K} costs={costs}")
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_cases(fg, handle, oracle):
     rng = synth.rng_for(31)
