@@ -1274,13 +1274,18 @@ int fastged_solve_batch(fastged_handle_t *h, int32_t npairs, const fastged_graph
         // queue behind the previous one's.  Pairs are independent: chunking changes no result.
         std::vector<std::pair<int32_t, int32_t>> cuts; // (first pair, count)
         {
-            int32_t start = 0, sz = npairs >= PIPELINE_MIN_PAIRS ? std::max<int32_t>(npairs / 16, 512) : npairs;
+            // first chunk npairs / div, then growth x g (tuning knobs FASTGED_PIPE_DIV / FASTGED_PIPE_GROWTH)
+            static const int div = [] { const char *e = getenv("FASTGED_PIPE_DIV"); return e ? std::max(1, atoi(e)) : 16; }();
+            static const double grow = [] { const char *e = getenv("FASTGED_PIPE_GROWTH"); return e ? std::max(1.1, atof(e)) : 2.0; }();
+            int32_t start = 0;
+            double szd = npairs >= PIPELINE_MIN_PAIRS ? std::max<double>(npairs / div, 256) : npairs;
             while (start < npairs) {
+                const int32_t sz = (int32_t)std::max(1.0, szd);
                 int32_t n = std::min<int32_t>(sz, npairs - start);
                 if (npairs - start - n < sz / 2) n = npairs - start; // no small tail chunk
                 cuts.push_back({start, n});
                 start += n;
-                sz *= 2;
+                szd *= grow;
             }
             if (cuts.empty()) cuts.push_back({0, 0});
         }
