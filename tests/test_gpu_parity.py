@@ -283,6 +283,18 @@ def test_random_torture(fg, handle, oracle):
         assert_batch_parity(fg, handle, oracle, pairs, costs, K, f"torture K={K} costs={costs}")
 
 
+def test_package_entry_points(fg, oracle):
+    """paper_2605_00830_b200.ged / ged_batch (convenience wrappers over the C ABI) give the oracle's results."""
+    import paper_2605_00830_b200 as pkg
+    w = synth.config_workload(2, npairs=20)
+    pairs = [w.pair(k) for k in range(w.npairs)]
+    c, maps = pkg.ged_batch(pairs, w.costs, K=w.K)
+    oc, om, _ = oracle.kbest_batch(pairs, w.costs, w.K)
+    assert np.array_equal(c, oc) and all(np.array_equal(x, y) for x, y in zip(maps, om))
+    r = pkg.ged(*pairs[0], w.costs, K=w.K)
+    assert r["cost"] == oc[0] and np.array_equal(r["mapping"], om[0])
+
+
 # ------------------------------------------------------------------ edge cases
 def test_edge_cases(fg, handle, oracle):
     rng = synth.rng_for(31)
