@@ -43,13 +43,16 @@ struct ShardArgs {
 
 // Status computed on the device from the reduced histogram (read by the host for control flow).
 struct ShardStatus {
-    int32_t keepall, tcode, r, retry, below_add, pad;
+    int32_t keepall, tcode, r, retry, below_add, lo; // lo: the level's base PED (the previous level's minimum)
     long long ci;
 };
 
 template <typename MapT, bool LAB>
-__global__ void __launch_bounds__(256) sh_branch(const ShardArgs a, int i, int N, int base, int first) {
+// base = *lo_dev (the previous level's survivor minimum, left on the device by the min all-reduce: the host
+// does not wait for it) + base_off (the window slides of this level).
+__global__ void __launch_bounds__(256) sh_branch(const ShardArgs a, int i, int N, const int32_t *lo_dev, int base_off, int first) {
     extern __shared__ __align__(16) uint8_t dsm[];
+    const int base = *lo_dev + base_off;
     __shared__ int s_hist[256];
     __shared__ long long s_cnt;
     constexpr int NWB = 8;
@@ -149,10 +152,12 @@ __global__ void __launch_bounds__(256) sh_branch(const ShardArgs a, int i, int N
 }
 
 // Threshold from the globally reduced histogram (1 thread; identical on every rank).
-__global__ void sh_thresh(const int32_t *hist, const long long *ci, int K, int win, int below, ShardStatus *st) {
+__global__ void sh_thresh(const int32_t *hist, const long long *ci, int K, int win, int below, const int32_t *lo_dev,
+                          ShardStatus *st) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     ShardStatus s{};
     s.ci = *ci;
+    s.lo = *lo_dev;
     s.keepall = s.ci <= K;
     if (!s.keepall) {
         int cum = below, t = 0;
@@ -340,6 +345,21 @@ __global__ void reduce_totals(const int32_t *wlt, const int32_t *weq, int n, int
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { ta += s[0][w]; tb += s[1][w]; }
         tot[0] = ta;
         tot[1] = tb;
+    }
+}
+
+// Loopback "collective" of the virtual-shard transport: element-wise sum or min over the G shards' buffers
+// (all on this device), written back to every shard, with no host round trip.
+template <typename T>
+struct ShardPtrs {
+    T *p[16];
+};
+template <typename T, int OP> // OP 0 = sum, 1 = min
+__global__ void sh_combine(ShardPtrs<T> ps, int G, int n) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        T acc = ps.p[0][x];
+        for (int g = 1; g < G; ++g) acc = OP == 0 ? acc + ps.p[g][x] : (ps.p[g][x] < acc ? ps.p[g][x] : acc);
+        for (int g = 0; g < G; ++g) ps.p[g][x] = acc;
     }
 }
 
