@@ -312,8 +312,9 @@ def run_ours(args, rank, local_rank, world):
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof.get("bench_kernel_dram_bytes_per_launch", {}).get(args.workload) \
-            if isinstance(prof.get("bench_kernel_dram_bytes_per_launch"), dict) else None
+        # DRAM bytes of all batched launches of one step (ncu --set full of the same workload), the unit of
+        # roofline.achieved (algorithmic ops or bytes per step over the step's kernel time)
+        traffic = (prof.get("bench_kernel_dram_bytes_per_step") or {}).get(args.workload)
     except Exception:
         pass
     line = {

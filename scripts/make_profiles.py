@@ -42,7 +42,9 @@ valid = [d for d in dram if d is not None]
 summary = {"source": "ncu --set full --clock-control none -k regex:kbest_batch -c 3 python scripts/prof_batch.py 10000 1000 1 (the bench workload)",
            "kernels": [x['Kernel Name'] for x in recs], "dram_bytes_per_launch": dram,
            # DRAM bytes per launch of the batched kernels, keyed by bench workload (bench.py roofline.traffic)
-           "bench_kernel_dram_bytes_per_launch": {"cfg3": (sum(valid) / len(valid)) if valid else None}}
+           "bench_kernel_dram_bytes_per_launch": {"cfg3": (sum(valid) / len(valid)) if valid else None},
+           # all batched launches of one step (the word-width groups run concurrently): bench.py roofline.traffic
+           "bench_kernel_dram_bytes_per_step": {"cfg3": sum(valid) if valid else None}}
 if os.path.exists(f"{REP}/prof_cfg5.ncu-rep"):
     o5 = subprocess.run(["ncu", "-i", f"{REP}/prof_cfg5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r5 = list(csv.reader(o5.splitlines())); h5 = r5[0]; u5 = r5[1]
@@ -51,6 +53,7 @@ if os.path.exists(f"{REP}/prof_cfg5.ncu-rep"):
         i1, i2 = h5.index("dram__bytes_read.sum"), h5.index("dram__bytes_write.sum")
         vals.append((float(row[i1]) + float(row[i2])) * scale.get(u5[i1], 1))
     summary["bench_kernel_dram_bytes_per_launch"]["cfg5"] = sum(vals) / len(vals) if vals else None
+    summary["bench_kernel_dram_bytes_per_step"]["cfg5"] = sum(vals) if vals else None
     summary["cfg5_source"] = "ncu --set full --clock-control none -k regex:kbest_batch -c 2 python scripts/prof_cfg5.py 20000"
 if os.path.exists(f"{REP}/prof_large5.ncu-rep"):  # cfg4 bench launch (n=500 p=0.05 K=1e5)
     o2 = subprocess.run(["ncu", "-i", f"{REP}/prof_large5.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
