@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfastged.so")
 SRCS = [os.path.join(HERE, "csrc", "fastged.cu")]
-DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "large_kernel.cuh", "shard_kernels.cuh",
+DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("batch_kernel.cuh", "large_kernel.cuh",
                                                        "shard_host.inc", "editpath.inc")] + \
     [os.path.join(ROOT, "include", "fastged.h")]
 

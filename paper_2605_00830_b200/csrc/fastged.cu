@@ -23,7 +23,6 @@
 #include "../../include/fastged.h"
 #include "batch_kernel.cuh"
 #include "large_kernel.cuh"
-#include "shard_kernels.cuh"
 
 namespace {
 
@@ -173,7 +172,10 @@ struct fastged_handle {
     DevBuf lblob, lbuf; // large single-pair mode
     fastged_batch *tmp = nullptr;        // reused by solve_batch (first chunk) / solve_pair
     std::vector<fastged_batch *> tmpv;  // reused by solve_batch (later pipelined chunks)
-    ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1, NCCL transport)
+    ncclComm_t comm = nullptr;    // sharded single-pair mode (world_size > 1): bootstrap and barriers
+    DevBuf xbuf;                  // NCCL staging (IPC handles, barrier word)
+    std::vector<std::vector<uint8_t>> peer_handle; // [world] CUDA IPC handle of each peer's lbuf
+    std::vector<void *> peer_base;                 // [world] its mapping here (NULL: not mapped)
     // batched launches of the word-width groups run concurrently (fork/join on side streams), so the
     // tail of one group's persistent launch overlaps the next group's start
     std::vector<cudaStream_t> gstreams;
@@ -548,7 +550,7 @@ struct LargeDst {
 };
 void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
                  const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
-                 const LargeDst *dst = nullptr);
+                 const LargeDst *dst = nullptr, bool sharded = false);
 
 // A pair rebuilt from its packed form in the batch's staging (vertex labels as given, edge labels
 // as the interned ids of pack_pair -- equal ids exactly where the original labels are equal, which is
@@ -892,10 +894,21 @@ void begin_call(fastged_handle_t *h) {
 }
 
 
+#include "shard_host.inc"
+
 void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
                  const fastged_costs_t *c, int64_t k, fastged_result_t *out, int64_t *levels_out,
-                 const LargeDst *dst) {
-    NvtxRange nv("fastged: whole-GPU pair");
+                 const LargeDst *dst, bool sharded) {
+    NvtxRange nv(sharded ? "fastged: sharded pair" : "fastged: whole-GPU pair");
+    // sharded single pair: G ranks, each a cooperative grid on its own GPU (peer
+    // memory over NVLink), or -- FASTGED_FLAG_VIRTUAL_SHARDS -- G CTA groups of one grid on this GPU
+    const int G = sharded ? h->world : 1;
+    const bool virt = sharded && (h->flags & FASTGED_FLAG_VIRTUAL_SHARDS);
+    const bool real = G > 1 && !virt;
+    const int myrank = real ? h->rank : 0;
+    if (G > FG_MAXG) fail(FASTGED_ERR_ARG, "sharded mode supports at most %d ranks", FG_MAXG);
+    if (real && !h->comm) fail(FASTGED_ERR_NCCL, "the handle's NCCL communicator was aborted by an earlier failure");
+    if (dst && G > 1) fail(FASTGED_ERR_ARG, "internal: a batch pair is never sharded");
     const int n1 = g1->n, n2 = g2->n;
     if (h->flags & FASTGED_FLAG_LAST_BY_TOTAL)
         fail(FASTGED_ERR_ARG, "FASTGED_FLAG_LAST_BY_TOTAL is implemented on the batched path only (n2 <= 128)");
@@ -965,7 +978,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     size_t static_smem = 0;
     {
         cudaFuncAttributes fa;
-        CK(cudaFuncGetAttributes(&fa, (const void *)fg::kbest_large_kernel<uint16_t, uint16_t, true>));
+        CK(cudaFuncGetAttributes(&fa, (const void *)fg::kbest_large_kernel<uint16_t, uint16_t, true, true>));
         static_smem = fa.sharedSizeBytes;
     }
     const size_t smem_cap = (size_t)h->smem_optin - static_smem;
@@ -980,7 +993,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const size_t smem = fg::large_smem_bytes(cs, csz, n1s, esz, nwa, n1r, W, n2, nnbr, adjT_in_smem, csr_in_smem);
     if (smem > smem_cap) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
     void *kfn = nullptr;
-#define LK(M, C, L) (void *)fg::kbest_large_kernel<M, C, L>
+#define LK(M, C, L) (sharded ? (void *)fg::kbest_large_kernel<M, C, L, true> : (void *)fg::kbest_large_kernel<M, C, L, false>)
     if (wide) kfn = c16 ? (lab ? LK(uint16_t, uint16_t, true) : LK(uint16_t, uint16_t, false))
                         : (lab ? LK(uint16_t, uint8_t, true) : LK(uint16_t, uint8_t, false));
     else kfn = c16 ? (lab ? LK(uint8_t, uint16_t, true) : LK(uint8_t, uint16_t, false))
@@ -991,31 +1004,67 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, fg::LNT, smem));
     if (occ < 1) fail(FASTGED_ERR_CAPACITY, "large-mode kernel does not fit on an SM (smem %zu)", smem);
     occ = 1; // one CTA per SM (the grid barrier cost grows with the CTA count)
-    const int grid = occ * h->sms;
-    const int GW = grid * (fg::LNT / 32);
-    if (grid > fg::LMAXGRID) fail(FASTGED_ERR_ARG, "large-mode grid %d exceeds %d CTAs", grid, fg::LMAXGRID);
-    // device buffers
+    const int nb = virt ? h->sms / G : occ * h->sms; // CTAs per rank
+    if (nb < 1) fail(FASTGED_ERR_ARG, "%d virtual shards on %d SMs", G, h->sms);
+    const int grid = virt ? G * nb : nb;
+    const int GW = nb * (fg::LNT / 32); // warps per rank
+    if (nb > fg::LMAXGRID) fail(FASTGED_ERR_ARG, "large-mode grid %d exceeds %d CTAs", nb, fg::LMAXGRID);
+    // device buffers: the home arrays (used on rank 0 only), then one rank-local block per rank held
+    // here (G blocks in virtual mode); a rank's slice of a level holds at most ceil(Kc / G) nodes
+    const size_t Kl = (size_t)((Kc + G - 1) / G);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
-    size_t o_ped0 = take(4 * (size_t)Kc), o_ped1 = take(4 * (size_t)Kc);
-    size_t o_used0 = take(4 * (size_t)Kc * W), o_used1 = take(4 * (size_t)Kc * W);
-    size_t o_cnt0 = take((size_t)csz * cs * Kc), o_cnt1 = take((size_t)csz * cs * Kc);
-    size_t o_map0 = take((size_t)esz * n1s * Kc), o_map1 = take((size_t)esz * n1s * Kc);
-    size_t o_codes = take((size_t)Kc * cs), o_selp = take(4 * (size_t)Kc), o_selj = take(4 * (size_t)Kc);
-    size_t o_selped = take(4 * (size_t)Kc);
-    size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1));
-    size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
-    size_t o_wlt = take(4 * (size_t)GW), o_weq = take(4 * (size_t)GW), o_best = take(8), o_out = take(80);
-    size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
-    size_t o_ctl = take(4 * (size_t)grid), o_cte = take(4 * (size_t)grid), o_rowc = take(4 * (size_t)Kc);
-    size_t o_rowpl = take(4 * (size_t)Kc), o_rowpe = take(4 * (size_t)Kc), o_rowmin = take(4 * (size_t)Kc);
-    CK(h->lbuf.reserve(off));
+    const size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1));
+    const size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
+    const size_t o_ctl = take(4 * (size_t)G * nb), o_cte = take(4 * (size_t)G * nb);
+    const size_t o_best = take(8), o_bar = take(4), o_out = take(80);
+    const size_t o_mapout = take(4 * (size_t)(n1 + 1)), o_lev = take(24 * (size_t)(n1 + 1));
+    const size_t o_rk = take(sizeof(fg::LargeArgs::Rank) * FG_MAXG), o_xerr = take(4);
+    const size_t home_bytes = off;
+    off = 0;
+    const size_t l_ped0 = take(4 * Kl), l_ped1 = take(4 * Kl);
+    const size_t l_used0 = take(4 * Kl * W), l_used1 = take(4 * Kl * W);
+    const size_t l_cnt0 = take((size_t)csz * cs * Kl), l_cnt1 = take((size_t)csz * cs * Kl);
+    const size_t l_map0 = take((size_t)esz * n1s * Kl), l_map1 = take((size_t)esz * n1s * Kl);
+    const size_t l_codes = take(Kl * cs), l_selp = take(4 * Kl), l_selj = take(4 * Kl), l_selped = take(4 * Kl);
+    const size_t l_rowc = take(4 * Kl), l_rowpl = take(4 * Kl), l_rowpe = take(4 * Kl), l_rowmin = take(4 * Kl);
+    const size_t l_wlt = take(4 * (size_t)GW), l_weq = take(4 * (size_t)GW);
+    const size_t local_bytes = off;
+    const int nloc = virt ? G : 1; // rank-local blocks in this process
+    CK(h->lbuf.reserve(home_bytes + (size_t)nloc * local_bytes));
     uint8_t *B = (uint8_t *)h->lbuf.p;
-    CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
-    CK(cudaMemsetAsync(B + o_ci, 0, 8 * (size_t)(n1 + 1), h->stream));
-    CK(cudaMemsetAsync(B + o_lo, 0x7f, 4 * (size_t)(n1 + 2), h->stream));
-    CK(cudaMemsetAsync(B + o_hi, 0x80, 4 * (size_t)(n1 + 2), h->stream));
-    CK(cudaMemsetAsync(B + o_best, 0xff, 8, h->stream));
+    // base address of every rank's buffer (real mode: peers' buffers mapped over NVLink)
+    std::vector<uint8_t *> rbase(G, nullptr);
+    if (real) {
+        ipc_map_peers(h, B, rbase);
+    } else {
+        rbase[0] = B;
+    }
+    uint8_t *H = rbase[0]; // home arrays (rank 0)
+    std::vector<fg::LargeArgs::Rank> rk(FG_MAXG);
+    for (int r = 0; r < G; ++r) {
+        uint8_t *L = virt ? B + home_bytes + (size_t)r * local_bytes : rbase[real ? r : 0] + home_bytes;
+        fg::LargeArgs::Rank &x = rk[r];
+        x.ped[0] = (int32_t *)(L + l_ped0); x.ped[1] = (int32_t *)(L + l_ped1);
+        x.used[0] = (uint32_t *)(L + l_used0); x.used[1] = (uint32_t *)(L + l_used1);
+        x.cnt[0] = L + l_cnt0; x.cnt[1] = L + l_cnt1;
+        x.map[0] = L + l_map0; x.map[1] = L + l_map1;
+        x.codes = L + l_codes;
+        x.sel_p = (int32_t *)(L + l_selp); x.sel_j = (int32_t *)(L + l_selj); x.sel_ped = (int32_t *)(L + l_selped);
+        x.rowc = (int32_t *)(L + l_rowc); x.rowpl = (int32_t *)(L + l_rowpl); x.rowpe = (int32_t *)(L + l_rowpe);
+        x.rowmin = (int32_t *)(L + l_rowmin);
+        x.wlt = (int32_t *)(L + l_wlt); x.weq = (int32_t *)(L + l_weq);
+    }
+    CK(cudaMemcpyAsync(B + o_rk, rk.data(), sizeof(fg::LargeArgs::Rank) * FG_MAXG, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(B + o_xerr, 0, 4, h->stream));
+    if (myrank == 0) { // the home arrays (only rank 0's are read)
+        CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
+        CK(cudaMemsetAsync(B + o_ci, 0, 8 * (size_t)(n1 + 1), h->stream));
+        CK(cudaMemsetAsync(B + o_lo, 0x7f, 4 * (size_t)(n1 + 2), h->stream));
+        CK(cudaMemsetAsync(B + o_hi, 0x80, 4 * (size_t)(n1 + 2), h->stream));
+        CK(cudaMemsetAsync(B + o_best, 0xff, 8, h->stream));
+        CK(cudaMemsetAsync(B + o_bar, 0, 4, h->stream));
+    }
     const uint8_t *dblob = (const uint8_t *)h->lblob.p;
     fg::LargeArgs a{};
     a.blob = dblob;
@@ -1036,23 +1085,25 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.nptr = (const int32_t *)(dblob + o_nptr);
     a.nbr = (const uint32_t *)(dblob + o_nbr);
     a.adjT = (const uint32_t *)(dblob + o_adjT);
-    a.ped[0] = (int32_t *)(B + o_ped0); a.ped[1] = (int32_t *)(B + o_ped1);
-    a.used[0] = (uint32_t *)(B + o_used0); a.used[1] = (uint32_t *)(B + o_used1);
-    a.cnt[0] = B + o_cnt0; a.cnt[1] = B + o_cnt1;
-    a.map[0] = B + o_map0; a.map[1] = B + o_map1;
-    a.codes = B + o_codes;
-    a.sel_p = (int32_t *)(B + o_selp); a.sel_j = (int32_t *)(B + o_selj); a.sel_ped = (int32_t *)(B + o_selped);
-    a.hist = (int32_t *)(B + o_hist);
-    a.ci = (int64_t *)(B + o_ci);
-    a.lo = (int32_t *)(B + o_lo);
-    a.hi = (int32_t *)(B + o_hi);
-    a.wlt = (int32_t *)(B + o_wlt); a.weq = (int32_t *)(B + o_weq);
-    a.ctl = (int32_t *)(B + o_ctl); a.cte = (int32_t *)(B + o_cte); a.rowc = (int32_t *)(B + o_rowc);
-    a.rowpl = (int32_t *)(B + o_rowpl); a.rowpe = (int32_t *)(B + o_rowpe); a.rowmin = (int32_t *)(B + o_rowmin);
-    a.best = (unsigned long long *)(B + o_best);
-    a.out = (int64_t *)(B + o_out);
-    a.map_out = (int32_t *)(B + o_mapout);
-    a.levels_out = levels_out ? (int64_t *)(B + o_lev) : nullptr;
+    a.G = G;
+    a.nb = nb;
+    a.rank = myrank;
+    a.virt = virt ? 1 : 0;
+    a.rk = (const fg::LargeArgs::Rank *)(B + o_rk);
+    a.self = rk[myrank];
+    a.vstride = virt ? (int64_t)local_bytes : 0;
+    a.hist = (int32_t *)(H + o_hist);
+    a.ci = (int64_t *)(H + o_ci);
+    a.lo = (int32_t *)(H + o_lo);
+    a.hi = (int32_t *)(H + o_hi);
+    a.ctl = (int32_t *)(H + o_ctl); a.cte = (int32_t *)(H + o_cte);
+    a.best = (unsigned long long *)(H + o_best);
+    a.bar = (unsigned int *)(H + o_bar);
+    a.xerr = (int32_t *)(B + o_xerr);
+    a.xtimeout_ns = (int64_t)(nccl_timeout_s() * 1e9);
+    a.out = (int64_t *)(H + o_out);
+    a.map_out = (int32_t *)(H + o_mapout);
+    a.levels_out = levels_out ? (int64_t *)(H + o_lev) : nullptr;
     void *params[] = {(void *)&a};
     if (dst) { // inside a batch: enqueue only, results stay on the device (stream-ordered copies)
         cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1074,17 +1125,25 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     }
     h->evused = 0;
     cudaEvent_t e0 = next_event(h), e1 = next_event(h);
+    // real mode: every rank's home/local initialisation is done before any rank's kernel starts (and,
+    // below, every kernel is done before any rank reuses its buffers): an NCCL barrier on the stream
+    if (real) nccl_stream_barrier(h);
     CK(cudaEventRecord(h->ev_begin, h->stream));
     CK(cudaEventRecord(e0, h->stream));
     CK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(fg::LNT), params, smem, h->stream));
     CK(cudaEventRecord(e1, h->stream));
     CK(cudaEventRecord(h->ev_end, h->stream));
+    if (real) nccl_stream_barrier(h);
     h->stats.kernel_launches = 1;
     int64_t res[10];
-    CK(cudaMemcpyAsync(res, a.out, 80, cudaMemcpyDeviceToHost, h->stream));
-    if (n1) CK(cudaMemcpyAsync(out->mapping, a.map_out, 4 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
-    if (levels_out && n1) CK(cudaMemcpyAsync(levels_out, a.levels_out, 24 * (size_t)n1, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    int32_t xerr = 0;
+    CK(cudaMemcpyAsync(res, a.out, 80, cudaMemcpyDefault, h->stream));
+    CK(cudaMemcpyAsync(&xerr, a.xerr, 4, cudaMemcpyDeviceToHost, h->stream));
+    if (n1) CK(cudaMemcpyAsync(out->mapping, a.map_out, 4 * (size_t)n1, cudaMemcpyDefault, h->stream));
+    if (levels_out && n1) CK(cudaMemcpyAsync(levels_out, a.levels_out, 24 * (size_t)n1, cudaMemcpyDefault, h->stream));
+    if (real) nccl_stream_wait(h);
+    else CK(cudaStreamSynchronize(h->stream));
+    if (xerr) fail(FASTGED_ERR_NCCL, "a peer rank did not reach the in-kernel exchange barrier within %.0f s", nccl_timeout_s());
     float ms = 0.f, kms = 0.f;
     CK(cudaEventElapsedTime(&ms, h->ev_begin, h->ev_end));
     CK(cudaEventElapsedTime(&kms, e0, e1));
@@ -1104,7 +1163,6 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     out->device_ms = ms;
 }
 
-#include "shard_host.inc"
 #include "editpath.inc"
 
 } // namespace
@@ -1180,7 +1238,11 @@ void fastged_destroy(fastged_handle_t *h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (void *p : h->peer_base)
+        if (p) cudaIpcCloseMemHandle(p);
+    h->peer_base.clear();
     if (h->comm) ncclCommDestroy(h->comm);
+    h->xbuf.release();
     h->lblob.release();
     h->lbuf.release();
     free_batch(h->tmp);

@@ -56,7 +56,10 @@ constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per 
 #define FG_LPF 2
 #endif
 constexpr int LPF = FG_LPF;   // per-warp prefetch ring: the next parent's rows in flight while one is expanded
-constexpr int LMAXGRID = 256; // CTAs of the large kernel (one per SM)
+constexpr int LMAXGRID = 256; // CTAs of the large kernel per rank (one per SM)
+#ifndef FG_MAXG
+#define FG_MAXG 8 // ranks of the sharded single-pair mode (one 8-GPU node)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cpa4(void *sdst, const void *gsrc) {
@@ -126,21 +129,40 @@ struct LargeArgs {
     const int32_t *nptr;    // CSR of g2: [n2 + 1]
     const uint32_t *nbr;    // [2 m2]: neighbour | (edge label id << 16)
     const uint32_t *adjT;   // [W][cs]: bit (u' & 31) of adjT[w][u] = edge (u, 32 w + u')
-    int32_t *ped[2];        // [Kc]      PED of the nodes of a level
-    uint32_t *used[2];      // [Kc][W]   rows of the nodes of level L live in buffer L & 1
-    void *cnt[2];           // [Kc][cs] CntT
-    void *map[2];           // [Kc][n1s] MapT
-    uint8_t *codes;         // [Kc][cs]
-    int32_t *sel_p, *sel_j, *sel_ped; // survivors: parent position, target (n2 = deletion, -1 = root), PED
+    // Frontier sharding.  The G ranks hold contiguous, equal
+    // slices of every level's frontier: rank r owns the global positions [N r / G, N (r+1) / G).
+    // A node's rows live on its owner; a child whose parent lives on another rank reads the parent's
+    // rows through a peer pointer (NVLink), and the descriptors of the next level are written straight
+    // into the owner's arrays.  Histogram, counts, PED range and argmin go to the home arrays (rank 0's
+    // memory).  G = 1 is the single-GPU kernel.  virt: the G ranks are equal CTA groups of this one
+    // grid (one GPU; the exchange protocol is the same, only the barrier differs).
+    int32_t G, rank, virt;
+    int32_t nb;                 // CTAs per rank
+    struct Rank {
+        int32_t *ped[2];        // [Kl]      PED of the nodes of a level
+        uint32_t *used[2];      // [Kl][W]   rows of the nodes of level L live in buffer L & 1
+        void *cnt[2];           // [Kl][cs] CntT
+        void *map[2];           // [Kl][n1s] MapT
+        uint8_t *codes;         // [Kl][cs]
+        int32_t *sel_p, *sel_j, *sel_ped; // nodes of the next level: parent row on its rank; target
+                                          // (n2 = deletion, -1 = root; int16) | parent's rank << 16; PED
+        int32_t *rowc;          // [Kl] per parent row: (codes < t) | (codes == t) << 16
+        int32_t *rowpl, *rowpe; // [Kl] codes < t / == t in the rows of the same B range before this row
+        int32_t *rowmin;        // [Kl] smallest rank code of the row (A): B reads only rows that can hold survivors
+        int32_t *wlt, *weq;     // [warps of the rank] codes < t / == t in the CTA's B ranges before this warp's
+    };
+    const Rank *rk;             // [G] (device memory), indexed by rank; other ranks' arrays are peer-mapped
+    Rank self;                  // this rank's arrays (virtual mode: rank 0's; rank r's are at + r vstride bytes)
+    int64_t vstride;
+    // home arrays (rank 0)
     int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
     int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
-    int32_t *wlt, *weq;     // [total warps] codes < t / == t in the CTA's B ranges before this warp's
-    int32_t *ctl, *cte;     // [grid] the same per CTA
-    int32_t *rowc;          // [Kc] per parent row: (codes < t) | (codes == t) << 16
-    int32_t *rowpl, *rowpe; // [Kc] codes < t / == t in the rows of the same B range before this row
-    int32_t *rowmin;        // [Kc] smallest rank code of the row (A): B reads only rows that can hold survivors
+    int32_t *ctl, *cte;     // [G * CTAs per rank] codes < t / == t per CTA
     unsigned long long *best;
+    unsigned int *bar;      // cross-rank barrier counter (real multi-GPU mode)
+    int32_t *xerr;          // this rank's own flag: a peer missed a barrier for xtimeout_ns (the kernel returns)
+    int64_t xtimeout_ns;
     int64_t *out;           // [0] cost, [1] children, [2] parents, [3] algorithmic bytes,
                             // [4..8] ns in phases A+T, B, C1, -, finalize (CTA 0's clock),
                             // [9] children that entered the rank histogram
@@ -187,10 +209,15 @@ __device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, 
     return pedp + cv + c.edel * d + c.eins * cnt - (c.edel + c.eins) * cb + c.esub * mis;
 }
 
+template <typename T>
+__device__ __forceinline__ T *fg_loc(T *p, int64_t off) { return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + off); }
+
 #ifdef FG_LSTAT
 __device__ unsigned long long fg_lstat[2];
 #endif
-template <typename MapT, typename CntT, bool LAB>
+// SHARD = false: one GPU (G = 1); every sharding quantity folds to a constant, so the single-GPU
+// kernel carries no register cost for the sharded mode.
+template <typename MapT, typename CntT, bool LAB, bool SHARD>
 __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     constexpr int NWB = LNT / 32;
@@ -200,11 +227,73 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     __shared__ int s_cpre[2][LMAXGRID]; // exclusive prefix of the per-CTA counts
     __shared__ long long s_cnt;
     __shared__ int s_next; // A: next parent of this CTA's range (warps take parents dynamically)
+    __shared__ LargeArgs::Rank s_rk[FG_MAXG]; // the ranks' array pointers (a.rk), dynamically indexed
     cg::grid_group grid = cg::this_grid();
     using C4 = Cnt4<CntT>;
 
+    // rank of this CTA and its index among the rank's CTAs (virtual mode: equal CTA groups).  Kept in
+    // shared memory and re-read where used (volatile): the branch loop's registers are all taken.
+    __shared__ int s_rank, s_lb;
+    __shared__ long long s_roff;
+    __shared__ unsigned int s_xepoch;
+    const int G = SHARD ? a.G : 1, nb = SHARD ? a.nb : (int)gridDim.x;
+    if (threadIdx.x == 0) {
+        const int r = a.virt ? (int)blockIdx.x / nb : a.rank;
+        s_rank = r;
+        s_lb = a.virt ? (int)blockIdx.x % nb : (int)blockIdx.x;
+        // this rank's own arrays: kernel parameters, offset by the rank's block in virtual mode
+        s_roff = a.virt ? (long long)r * a.vstride : 0;
+        s_xepoch = 0;
+    }
+    if (SHARD)
+        for (int x = threadIdx.x; x < G * (int)(sizeof(LargeArgs::Rank) / 8); x += LNT)
+            reinterpret_cast<unsigned long long *>(s_rk)[x] = reinterpret_cast<const unsigned long long *>(a.rk)[x];
+    block_sync();
+#define RANK (SHARD ? s_rank : 0)
+#define LB (SHARD ? s_lb : (int)blockIdx.x)
+#define ML(f) (SHARD ? fg_loc(a.self.f, s_roff) : a.self.f)
+    // field f of rank r's arrays (a peer's memory when sharded)
+#define RK(r, f) (SHARD ? s_rk[r].f : a.self.f)
+    // the one CTA that writes the home-only outputs
+    auto home0 = [&]() { return RANK == 0 && LB == 0; };
+    // slice of a level of n nodes owned by rank r: [rstart(n, r), rstart(n, r + 1)); owner of position k
+    auto rstart = [&](int n, int r) -> int { return (int)(((int64_t)n * r) / G); };
+    auto rowner = [&](int k, int n) -> int { return G == 1 ? 0 : (int)((((int64_t)k + 1) * G - 1) / n); };
+    // a descriptor's target and the rank holding its parent's row
+    auto dtarget = [](int32_t v) -> int { return (int)(int16_t)(v & 0xffff); };
+    auto drank = [](int32_t v) -> int { return (int)((uint32_t)v >> 16); };
+    // barrier over every CTA of every rank.  Virtual ranks share the grid; real ranks (one GPU each)
+    // meet at a counter in rank 0's memory after their own grid barrier (system-scope release/acquire:
+    // the remote descriptor writes and home atomics of every CTA are visible past it)
+    // Returns false (on every CTA of the rank) when a peer did not arrive within xtimeout_ns.
+    auto xsync = [&]() -> bool {
+        if (SHARD && G > 1 && !a.virt) __threadfence_system();
+        block_sync();
+        grid.sync();
+        if (SHARD && G > 1 && !a.virt) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                const unsigned xepoch = (s_xepoch += (unsigned)G);
+                atomicAdd_system(a.bar, 1u);
+                uint64_t t0, t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                for (;;) {
+                    unsigned v;
+                    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+                    if ((int)(v - xepoch) >= 0) break;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if ((int64_t)(t - t0) > a.xtimeout_ns) { *(volatile int32_t *)a.xerr = 1; break; }
+                    __nanosleep(256);
+                }
+            }
+            block_sync();
+            grid.sync();
+            return *(volatile int32_t *)a.xerr == 0;
+        }
+        return true;
+    };
+
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gw = blockIdx.x * NWB + wib, GW = gridDim.x * NWB;
+    const int gw = LB * NWB + wib, GW = nb * NWB; // warps of this rank
     const Costs c = a.c;
     const PairDesc pd = a.pd;
     const int n1 = pd.n1, n2 = pd.n2, W = a.W, K = a.K, win = a.win, cs = a.cs, S = a.S;
@@ -251,21 +340,21 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     auto adjw = [&](int j, int w) -> uint32_t { // word w of g2's bit row j
         return a.adjT_in_smem ? adjT[w * cs + j] : __ldg(adj2 + (int64_t)j * W + w);
     };
-    // root: lambda empty, nothing used, PED 0 -- row 0 of level -1 (buffer 1)
-    if (blockIdx.x == 0) {
-        if (threadIdx.x == 0) { a.sel_p[0] = 0; a.sel_j[0] = -1; a.sel_ped[0] = 0; }
-        for (int w = threadIdx.x; w < W; w += LNT) a.used[1][w] = 0u;
-        for (int u = threadIdx.x; u < cs; u += LNT) reinterpret_cast<CntT *>(a.cnt[1])[u] = 0;
+    // root: lambda empty, nothing used, PED 0 -- row 0 of level -1 (buffer 1), and the
+    // descriptor of the level-0 node; both live on the owner of position 0 of a one-node level
+    if (RANK == rowner(0, 1) && LB == 0) {
+        if (threadIdx.x == 0) { ML(sel_p)[0] = 0; ML(sel_j)[0] = 0xffff | (RANK << 16); ML(sel_ped)[0] = 0; }
+        for (int w = threadIdx.x; w < W; w += LNT) ML(used[1])[w] = 0u;
+        for (int u = threadIdx.x; u < cs; u += LNT) reinterpret_cast<CntT *>(ML(cnt[1]))[u] = 0;
     }
-    block_sync();
-    grid.sync();
+    if (!xsync()) return;
 
     int N = 1, lo = 0, hi = 0, ps = 0;
     int64_t children = 0, parents = 0, algb = 0;
     int64_t tph[5] = {0, 0, 0, 0, 0}, nhist = 0;
     uint64_t tlast = 0;
     auto tick = [&](int ph) { // phase clock (thread 0 of CTA 0, after a grid barrier)
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (home0() && threadIdx.x == 0) {
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             if (ph >= 0) tph[ph] += (int64_t)(t - tlast);
@@ -275,12 +364,11 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     tick(-1);
     for (int i = 0; i < n1; ++i) {
         const int pv = (i + 1) & 1, cu = i & 1; // buffers of level i-1 (the parents' parents) and level i
-        const uint32_t *Pused = a.used[pv];
-        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[pv]);
-        const MapT *Pmap = reinterpret_cast<const MapT *>(a.map[pv]);
-        uint32_t *Qused = a.used[cu];
-        CntT *Qcnt = reinterpret_cast<CntT *>(a.cnt[cu]);
-        MapT *Qmap = reinterpret_cast<MapT *>(a.map[cu]);
+        // this rank's nodes of level i: global positions [s0, s0 + Nl), local rows 0..Nl-1
+        const int s0 = rstart(N, RANK), Nl = rstart(N, RANK + 1) - s0;
+        uint32_t *Qused = ML(used[cu]);
+        CntT *Qcnt = reinterpret_cast<CntT *>(ML(cnt[cu]));
+        MapT *Qmap = reinterpret_cast<MapT *>(ML(map[cu]));
         const int pbeg = __ldg(pptr + i), d = __ldg(pptr + i + 1) - pbeg;
         for (int k = threadIdx.x; k < d; k += LNT) {
             s_pq[k] = __ldg(pqg + pbeg + k);
@@ -297,10 +385,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         const int edd = c.edel * d, ee = c.edel + c.eins, pedDel = c.vdel + edd;
         // cB by scatter over neighbour lists, or by popcount over the nonzero words of B_p (uniform choice)
         const bool scatter = LAB || (d * a.degw * 8 < S * min(W, d) * 13);
-        const int chunk = (N + GW - 1) / GW; // B / C1: static contiguous code ranges per warp
-        const int p0 = min(N, gw * chunk), p1 = min(N, p0 + chunk);
-        const int cchunk = (N + gridDim.x - 1) / gridDim.x; // A: this CTA's parents, taken dynamically
-        const int cb0 = min(N, (int)blockIdx.x * cchunk), cb1 = min(N, cb0 + cchunk);
+        const int chunk = (Nl + GW - 1) / GW; // B / C1: static contiguous code ranges per warp (local rows)
+        const int p0 = min(Nl, gw * chunk), p1 = min(Nl, p0 + chunk);
+        const int cchunk = (Nl + nb - 1) / nb; // A: this CTA's parents, taken dynamically
+        const int cb0 = min(Nl, LB * cchunk), cb1 = min(Nl, cb0 + cchunk);
         constexpr int EPW = 4 / ESZ;                            // lambda entries per 32-bit word
         const int wprev = i > 0 ? (i - 1 + EPW - 1) / EPW : 0; // lambda words of a level-(i-1) row (entries 0..i-2)
         const int wcur = (i + EPW - 1) / EPW;                   // ... of a level-i row (entries 0..i-1)
@@ -315,7 +403,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             const int capc = (N >= K) ? max(0, min(win, hi + pedDel - base + 1)) : win;
             for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
             if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; }
-            if (blockIdx.x == 0)
+            if (home0())
                 for (int k = threadIdx.x; k < 256; k += LNT) a.hist[((ps + 1) % 3) * 256 + k] = 0;
             block_sync();
             int wcount = 0;
@@ -327,19 +415,21 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     if (lane == 0) v = atomicAdd(&s_next, 1);
                     return __shfl_sync(FULL, v, 0);
                 };
-                auto load_desc = [&](int k) -> int { // lanes 0..2: p, j, ped of parent k
+                auto load_desc = [&](int k) -> int { // lanes 0..2: p, j, ped of (local) node k
                     if (k >= cb1 || lane > 2) return 0;
-                    return lane == 0 ? a.sel_p[k] : (lane == 1 ? a.sel_j[k] : a.sel_ped[k]);
+                    return lane == 0 ? ML(sel_p)[k] : (lane == 1 ? ML(sel_j)[k] : ML(sel_ped)[k]);
                 };
                 auto issue = [&](int k, int dv, uint32_t *pf) {
-                    const int p = __shfl_sync(FULL, dv, 0);
+                    const int64_t pl = __shfl_sync(FULL, dv, 0); // the parent's row on its rank
+                    const int po = drank(__shfl_sync(FULL, dv, 1));
                     if (lane < 3) pf[PFW - 4 + 1 + lane] = (uint32_t)dv;
                     if (lane == 0) pf[PFW - 4] = (uint32_t)k;
                     if (k < cb1) {
-                        const uint8_t *crow8 = reinterpret_cast<const uint8_t *>(Pcnt + (int64_t)p * cs);
+                        // the parent's rows, on its rank (a peer's memory when sharded)
+                        const uint8_t *crow8 = reinterpret_cast<const uint8_t *>(reinterpret_cast<const CntT *>(RK(po, cnt[pv])) + pl * cs);
                         for (int x = lane; x < CNTW / 4; x += 32) cpa16(pf + 4 * x, crow8 + 16 * x);
-                        for (int w = lane; w < W; w += 32) cpa4(pf + CNTW + w, Pused + (int64_t)p * W + w);
-                        const uint32_t *mr = reinterpret_cast<const uint32_t *>(Pmap) + (int64_t)p * rowwords;
+                        for (int w = lane; w < W; w += 32) cpa4(pf + CNTW + w, RK(po, used[pv]) + pl * W + w);
+                        const uint32_t *mr = reinterpret_cast<const uint32_t *>(RK(po, map[pv])) + pl * rowwords;
                         for (int w = lane; w < wprev; w += 32) cpa4(pf + CNTW + 32 + w, mr + w);
                     }
                     cpa_commit(); // (possibly empty group: keeps the ring's group count uniform)
@@ -358,11 +448,11 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     uint32_t *pf = pfb + (r % LPF) * PFW;
                     const int k = (int)pf[PFW - 4];
                     if (k >= cb1) break; // (parents are taken in increasing order: the rest is empty)
-                    const int j = (int)pf[PFW - 2], pedp = (int)pf[PFW - 1];
+                    const int j = dtarget((int32_t)pf[PFW - 2]), pedp = (int)pf[PFW - 1];
                     const int jn = (j >= 0 && j < n2) ? j : -1; // target used by this node's last step
                     uint32_t *sU = pf + CNTW;
                     uint32_t *mrow = pf + CNTW + 32;
-                    if (lane == 0) a.ped[cu][k] = pedp;
+                    if (lane == 0) ML(ped[cu])[k] = pedp;
                     // materialise row k of level i: used | j, lambda + entry i-1, counters + adj2 row j
                     int nused = 0;
                     for (int w = lane; w < W; w += 32) {
@@ -423,7 +513,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     __syncwarp();
                     const int pb = pedp - base + 1 + edd;
                     const int cdel = rank_code(pedp + pedDel, base, win);
-                    uint8_t *crow = a.codes + (int64_t)k * cs;
+                    uint8_t *crow = ML(codes) + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
                     CntT *qc = Qcnt + (int64_t)k * cs;
                     uint32_t rmin = 255u;
@@ -470,7 +560,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         *reinterpret_cast<uint32_t *>(crow + u0) = word;
                     }
                     rmin = __reduce_min_sync(FULL, rmin);
-                    if (lane == 0) a.rowmin[k] = (int)rmin;
+                    if (lane == 0) ML(rowmin)[k] = (int)rmin;
                     wcount += n2 - nused + 1;
                     __syncwarp();
                 }
@@ -486,8 +576,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 if (v) atomicAdd(&gh[bin], v);
             }
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
-            block_sync();
-            grid.sync();
+            if (!xsync()) return;
             tick(0);
             // T: every CTA derives the same threshold from the global histogram
             const int64_t ci = a.ci[i];
@@ -508,7 +597,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         const int y = __shfl_up_sync(FULL, incl, o);
                         if (lane >= o) incl += y;
                     }
-                    if (blockIdx.x == 0 && lane == 31) nhist += incl;
+                    if (home0() && lane == 31) nhist += incl;
                     const unsigned hm = __ballot_sync(FULL, below + incl >= K);
                     if (hm) {
                         const int L = __ffs(hm) - 1;
@@ -549,7 +638,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             if (keepall) { mlt = ~bytes_eq(v, inv4) & 0x80808080u; meq = 0u; }
             else { mlt = bytes_lt(v, t4); meq = bytes_eq(v, t4); }
         };
-        auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(a.codes + (int64_t)k * cs)[x]; };
+        auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(ML(codes) + (int64_t)k * cs)[x]; };
         {
             int wl = 0, we = 0;
             // 32 rows per step, one per lane; only rows whose smallest code can be selected are read
@@ -557,7 +646,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             constexpr int BR = FG_LBR;
             for (int k0 = p0; k0 < p1; k0 += 32) {
                 const int kl = k0 + lane;
-                const bool q = kl < p1 && (keepall || a.rowmin[kl] <= tcode);
+                const bool q = kl < p1 && (keepall || ML(rowmin)[kl] <= tcode);
                 unsigned qm = __ballot_sync(FULL, q);
                 int myl = 0, mye = 0; // counts of row kl
                 while (qm) {
@@ -596,9 +685,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     if (lane >= o) { il += yl; ie += ye; }
                 }
                 if (kl < p1) {
-                    a.rowc[kl] = myl | (mye << 16);
-                    a.rowpl[kl] = wl + il - myl;
-                    a.rowpe[kl] = we + ie - mye;
+                    ML(rowc)[kl] = myl | (mye << 16);
+                    ML(rowpl)[kl] = wl + il - myl;
+                    ML(rowpe)[kl] = we + ie - mye;
                 }
                 wl += __shfl_sync(FULL, il, 31);
                 we += __shfl_sync(FULL, ie, 31);
@@ -608,32 +697,32 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             if (lane == 0) { // this warp's prefix inside the CTA
                 int cl = 0, ce = 0;
                 for (int w = 0; w < wib; ++w) { cl += s_red[0][w]; ce += s_red[1][w]; }
-                a.wlt[gw] = cl;
-                a.weq[gw] = ce;
-                if (wib == NWB - 1) { a.ctl[blockIdx.x] = cl + wl; a.cte[blockIdx.x] = ce + we; }
+                ML(wlt)[gw] = cl;
+                ML(weq)[gw] = ce;
+                if (wib == NWB - 1) { a.ctl[RANK * nb + LB] = cl + wl; a.cte[RANK * nb + LB] = ce + we; }
             }
         }
-        block_sync();
-        grid.sync();
+        if (!xsync()) return;
         tick(1);
 
         // ---------------- prefix of the per-CTA counts (every CTA, redundantly) ----------------
+        // CTAs in (rank, CTA) order = the global (parent, child) order; this rank's CTAs' prefixes kept
         if (wib == 0) {
-            int cl = 0, ce = 0, rl = 0, re = 0;
-            for (int g0 = 0; g0 < (int)gridDim.x; g0 += 32) {
+            const int gend = (RANK + 1) * nb, gme = RANK * nb;
+            int rl = 0, re = 0;
+            for (int g0 = 0; g0 < gend; g0 += 32) {
                 const int g = g0 + lane;
-                const int l = g < (int)gridDim.x ? a.ctl[g] : 0, e = g < (int)gridDim.x ? a.cte[g] : 0;
+                const int l = g < gend ? a.ctl[g] : 0, e = g < gend ? a.cte[g] : 0;
                 int il = l, ie = e;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int yl = __shfl_up_sync(FULL, il, o), ye = __shfl_up_sync(FULL, ie, o);
                     if (lane >= o) { il += yl; ie += ye; }
                 }
-                if (g < (int)gridDim.x) { s_cpre[0][g] = rl + il - l; s_cpre[1][g] = re + ie - e; }
+                if (g >= gme && g < gend) { s_cpre[0][g - gme] = rl + il - l; s_cpre[1][g - gme] = re + ie - e; }
                 rl += __shfl_sync(FULL, il, 31);
                 re += __shfl_sync(FULL, ie, 31);
             }
-            (void)cl; (void)ce;
         }
         block_sync();
         const int Nn = keepall ? (int)a.ci[i] : K;
@@ -648,24 +737,24 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             // 32 rows per batch (row kb + l GW for lane l): their counts and prefixes are loaded in parallel,
             // then the rows holding survivors are expanded one after the other, the next one's first code
             // vector already in flight (the loop is otherwise a chain of dependent global round trips)
-            for (int kb = gw; kb < N; kb += 32 * GW) {
+            for (int kb = gw; kb < Nl; kb += 32 * GW) {
                 const int kl = kb + lane * GW;
                 int rc = 0, lp = 0, ep = 0;
                 bool has = false;
-                if (kl < N) {
-                    rc = a.rowc[kl];
+                if (kl < Nl) {
+                    rc = ML(rowc)[kl];
                     has = keepall ? rc != 0 : ((rc & 0xffff) != 0 || (rc >> 16) > 0);
                     if (has) {
                         const int ow = kl / chunk, oc = ow / NWB;
-                        lp = s_cpre[0][oc] + a.wlt[ow] + a.rowpl[kl];
-                        ep = s_cpre[1][oc] + a.weq[ow] + a.rowpe[kl];
+                        lp = s_cpre[0][oc] + ML(wlt)[ow] + ML(rowpl)[kl];
+                        ep = s_cpre[1][oc] + ML(weq)[ow] + ML(rowpe)[kl];
                         if (!keepall && (rc & 0xffff) == 0 && ep >= rq) has = false; // its ties are all past the quota
                     }
                 }
                 unsigned hm = __ballot_sync(FULL, has);
 #ifdef FG_LSTAT
                 {
-                    const unsigned rows = __ballot_sync(FULL, kl < N);
+                    const unsigned rows = __ballot_sync(FULL, kl < Nl);
                     if (lane == 0) {
                         atomicAdd(&fg_lstat[0], (unsigned long long)__popc(hm));
                         atomicAdd(&fg_lstat[1], (unsigned long long)__popc(rows));
@@ -685,11 +774,11 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 for (int xb = 0; xb < vpr; xb += 32) {
                     const int x = xb + lane;
                     const uint4 v = xb == 0 ? v0 : (x < vpr ? rowvec(k, x) : inv);
-                    uint32_t ml[4], me[4];
-                    masks(v.x, ml[0], me[0]); masks(v.y, ml[1], me[1]);
-                    masks(v.z, ml[2], me[2]); masks(v.w, ml[3], me[3]);
+                    uint32_t ml[4], mq[4];
+                    masks(v.x, ml[0], mq[0]); masks(v.y, ml[1], mq[1]);
+                    masks(v.z, ml[2], mq[2]); masks(v.w, ml[3], mq[3]);
                     const int nlt = __popc(ml[0]) + __popc(ml[1]) + __popc(ml[2]) + __popc(ml[3]);
-                    const int neq = __popc(me[0]) + __popc(me[1]) + __popc(me[2]) + __popc(me[3]);
+                    const int neq = __popc(mq[0]) + __popc(mq[1]) + __popc(mq[2]) + __popc(mq[3]);
                     if (!__any_sync(FULL, (nlt | neq) != 0)) continue;
                     int einc = neq;
 #pragma unroll
@@ -711,7 +800,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         const uint32_t words[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                         for (int w = 0; w < 4; ++w) {
-                            uint32_t m = ml[w], e = me[w];
+                            uint32_t m = ml[w], e = mq[w];
                             while (e && ecnt < adm) { const uint32_t lowb = e & (0u - e); m |= lowb; e ^= lowb; ++ecnt; }
                             while (m) {
                                 const int by = (__ffs(m) - 1) >> 3;
@@ -722,11 +811,15 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                                 if (code >= 1 && code <= win) ped = base + code - 1;
                                 else // saturated code: recompute from the parent's materialised row (rare)
                                     ped = large_child_scalar<MapT, CntT, LAB>(
-                                        a, d, s_pq, s_pl, a.ped[cu][k], Qcnt + (int64_t)k * cs,
+                                        a, d, s_pq, s_pl, ML(ped[cu])[k], Qcnt + (int64_t)k * cs,
                                         Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
-                                a.sel_p[pos] = k;
-                                a.sel_j[pos] = u;
-                                a.sel_ped[pos] = ped;
+                                // the node of level i+1 at global position pos: its descriptor goes to its
+                                // owner (a peer when sharded); the parent is row k of this rank
+                                const int no = rowner(pos, Nn);
+                                const int np = pos - rstart(Nn, no);
+                                RK(no, sel_p)[np] = k;
+                                RK(no, sel_j)[np] = u | (RANK << 16);
+                                RK(no, sel_ped)[np] = ped;
                                 mylo = min(mylo, ped);
                                 myhi = max(myhi, ped);
                                 ++pos;
@@ -745,15 +838,14 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 atomicMax(&a.hi[i + 1], myhi);
             }
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0 && a.levels_out) {
+        if (home0() && threadIdx.x == 0 && a.levels_out) {
             a.levels_out[3 * i] = N;
             a.levels_out[3 * i + 1] = a.ci[i];
             a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
         }
         parents += N;
         algb += (int64_t)N * (4 + ESZ * d) + (int64_t)Nn * (ESZ * (2 * i + 1) + 8);
-        block_sync();
-        grid.sync();
+        if (!xsync()) return;
         tick(2);
         N = Nn;
         lo = a.lo[i + 1];
@@ -763,22 +855,24 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     // ---------------- finalize: completion + argmin ----------------
     {
         const int pv = (n1 + 1) & 1; // rows of level n1 - 1 (the final nodes' parents)
-        const uint32_t *Pused = a.used[pv];
-        const CntT *Pcnt = reinterpret_cast<const CntT *>(a.cnt[pv]);
-        for (int k = gw; k < N; k += GW) { // warp per final node (p, j)
-            const int p = a.sel_p[k], j = a.sel_j[k], ped = a.sel_ped[k];
+        const int s0 = rstart(N, RANK), Nl = rstart(N, RANK + 1) - s0;
+        for (int k = gw; k < Nl; k += GW) { // warp per final node (p, j) of this rank
+            const int64_t pl = ML(sel_p)[k];
+            const int po = drank(ML(sel_j)[k]), j = dtarget(ML(sel_j)[k]), ped = ML(sel_ped)[k];
+            const uint32_t *Pused = RK(po, used[pv]) + pl * W;
+            const CntT *Pcnt = reinterpret_cast<const CntT *>(RK(po, cnt[pv])) + pl * cs;
             const int jn = (j >= 0 && j < n2) ? j : -1;
             int usedc = 0, e2u2 = 0;
             for (int w = lane; w < W; w += 32) {
-                uint32_t uw = Pused[(int64_t)p * W + w];
+                uint32_t uw = Pused[w];
                 if (jn >= 0 && (jn >> 5) == w) uw |= 1u << (jn & 31);
                 usedc += __popc(uw);
             }
             for (int u = lane; u < n2; u += 32) {
-                uint32_t uw = Pused[(int64_t)p * W + (u >> 5)];
+                uint32_t uw = Pused[u >> 5];
                 if (jn >= 0 && (jn >> 5) == (u >> 5)) uw |= 1u << (jn & 31);
                 if ((uw >> (u & 31)) & 1u) {
-                    int cu = (int)Pcnt[(int64_t)p * cs + u];
+                    int cu = (int)Pcnt[u];
                     if (jn >= 0) cu += (int)((adjw(jn, u >> 5) >> (u & 31)) & 1u);
                     e2u2 += cu;
                 }
@@ -787,21 +881,22 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             e2u2 = __reduce_add_sync(FULL, e2u2); // every edge among used vertices counted from both ends
             if (lane == 0) {
                 const int64_t total = (int64_t)ped + (int64_t)c.vins * (n2 - usedc) + (int64_t)c.eins * (pd.m2 - e2u2 / 2);
-                atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)k);
+                atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)(s0 + k));
             }
         }
-        block_sync();
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 31) a.out[9] = nhist;
+        if (!xsync()) return;
+        if (home0() && threadIdx.x == 31) a.out[9] = nhist;
 #ifdef FG_LSTAT
-        if (blockIdx.x == 0 && threadIdx.x == 0)
+        if (home0() && threadIdx.x == 0)
             printf("LSTAT parents with a survivor %llu of %llu (%.3f)\n", fg_lstat[0], fg_lstat[1], (double)fg_lstat[0] / fg_lstat[1]);
 #endif
-        if (blockIdx.x == 0) {
+        if (home0()) {
             const unsigned long long best = *a.best;
             const int kb = (int)(best & 0xffffffffull);
-            const int p = a.sel_p[kb], j = a.sel_j[kb];
-            const MapT *row = reinterpret_cast<const MapT *>(a.map[pv]) + (int64_t)p * a.n1s;
+            const int ko = rowner(kb, N), kl = kb - rstart(N, ko);
+            const int64_t pl = RK(ko, sel_p)[kl];
+            const int po = drank(RK(ko, sel_j)[kl]), j = dtarget(RK(ko, sel_j)[kl]);
+            const MapT *row = reinterpret_cast<const MapT *>(RK(po, map[pv])) + pl * a.n1s;
             for (int q = threadIdx.x; q < n1; q += LNT) {
                 const int t = (q == n1 - 1) ? ((j == n2) ? DELV : j) : (int)row[q];
                 a.map_out[q] = (t == DELV) ? -1 : t;
@@ -817,5 +912,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         }
     }
 }
+#undef ML
+#undef RK
+#undef RANK
+#undef LB
 
 } // namespace fg

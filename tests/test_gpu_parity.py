@@ -470,9 +470,9 @@ def test_determinism_repeat(fg, handle):
 
 
 # ------------------------------------------------------------------ sharded single pair (§8 a6)
-@pytest.mark.parametrize("G", [1, 2, 3, 4])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
 def test_sharded_virtual_matches_oracle(fg, oracle, G):
-    """The frontier split by parent over G shards (loopback exchange on one GPU) gives the oracle's
+    """The frontier split over G virtual ranks (CTA groups of one grid, the in-kernel exchange) gives the oracle's
     cost, mapping, children count and per-level records for every G (bit-identical)."""
     flags = fg.FLAG_VIRTUAL_SHARDS
     hs = fg.Handle(0, world_size=G, flags=flags)
