@@ -52,8 +52,9 @@ extern "C" {
 #define FASTGED_FLAG_TIMING 1u      /* record CUDA events around every kernel launch (fastged_get_stats) */
 #define FASTGED_FLAG_DEBUG_WINDOW 2u /* test only: 2-wide rank window, forces the multi-pass rank path   */
 #define FASTGED_FLAG_FORCE_LARGE 4u  /* test only: solve_pair uses the whole-GPU path even for small pairs */
-#define FASTGED_FLAG_VIRTUAL_SHARDS 8u /* test only: world_size shards of one pair on this handle's GPU,
-                                         exchanged by device copies instead of NCCL (rank, nccl_id ignored) */
+#define FASTGED_FLAG_VIRTUAL_SHARDS 8u /* test only: world_size (<= 8) ranks of one pair as equal CTA groups
+                                         of one grid on this handle's GPU, the same in-kernel exchange as
+                                         real ranks (rank, nccl_id ignored)                              */
 #define FASTGED_FLAG_LAST_BY_TOTAL 16u /* method variant: rank the last level by
                                          PED + insertion completion instead of PED (the alternative to reading
                                          C10 of Alg. 1); never a higher cost than the
@@ -153,8 +154,13 @@ void fastged_destroy(fastged_handle_t *h);
 const char *fastged_last_error(const fastged_handle_t *h);
 
 /* K-Best GED of one pair (Alg. 1).  out->mapping must hold g1->n entries (may be
- * NULL when g1->n == 0).  Sharded mode (world_size > 1): a collective call; all ranks pass identical
- * inputs and receive the identical result.                                                     */
+ * NULL when g1->n == 0).  Sharded mode (world_size > 1, at most 8 ranks on one node, one GPU each,
+ * peer access over NVLink): a collective call; all ranks pass identical inputs and receive the
+ * identical result.  Each level's frontier is split into equal contiguous slices, one per rank; the
+ * per-level exchange (histogram, counts, the next level's node descriptors, the final argmin) runs
+ * inside the kernel over peer memory (CUDA IPC mappings set up over the NCCL communicator), with an
+ * in-kernel barrier across ranks.  A rank that fails, or a peer that misses a barrier for
+ * FASTGED_NCCL_TIMEOUT_S seconds (default 600), returns FASTGED_ERR_NCCL and aborts the communicator. */
 int fastged_solve_pair(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_graph_t *g2,
                        const fastged_costs_t *c, int64_t k, fastged_result_t *out);
 

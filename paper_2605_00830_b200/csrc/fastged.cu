@@ -1036,7 +1036,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     // base address of every rank's buffer (real mode: peers' buffers mapped over NVLink)
     std::vector<uint8_t *> rbase(G, nullptr);
     if (real) {
-        ipc_map_peers(h, B, rbase);
+        const int64_t key[2] = {(int64_t)nb, (int64_t)(home_bytes + local_bytes)};
+        ipc_map_peers(h, B, rbase, key);
     } else {
         rbase[0] = B;
     }
