@@ -1014,7 +1014,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const size_t Kl = (size_t)((Kc + G - 1) / G);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
-    const size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1));
+    const size_t o_hist = take(4 * 3 * 256), o_ci = take(8 * (size_t)(n1 + 1)), o_drop = take(4 * (size_t)(n1 + 1));
     const size_t o_lo = take(4 * (size_t)(n1 + 2)), o_hi = take(4 * (size_t)(n1 + 2));
     const size_t o_ctl = take(4 * (size_t)G * nb), o_cte = take(4 * (size_t)G * nb);
     const size_t o_best = take(8), o_bar = take(4), o_out = take(80);
@@ -1026,7 +1026,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const size_t l_used0 = take(4 * Kl * W), l_used1 = take(4 * Kl * W);
     const size_t l_cnt0 = take((size_t)csz * cs * Kl), l_cnt1 = take((size_t)csz * cs * Kl);
     const size_t l_map0 = take((size_t)esz * n1s * Kl), l_map1 = take((size_t)esz * n1s * Kl);
-    const size_t l_codes = take(Kl * cs), l_selp = take(4 * Kl), l_selj = take(4 * Kl), l_selped = take(4 * Kl);
+    const size_t l_ccode = take(Kl * cs), l_ctgt = take(2 * Kl * cs), l_rown = take(4 * Kl);
+    const size_t l_selp = take(4 * Kl), l_selj = take(4 * Kl), l_selped = take(4 * Kl);
     const size_t l_rowc = take(4 * Kl), l_rowpl = take(4 * Kl), l_rowpe = take(4 * Kl), l_rowmin = take(4 * Kl);
     const size_t l_wlt = take(4 * (size_t)GW), l_weq = take(4 * (size_t)GW);
     const size_t local_bytes = off;
@@ -1050,7 +1051,9 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
         x.used[0] = (uint32_t *)(L + l_used0); x.used[1] = (uint32_t *)(L + l_used1);
         x.cnt[0] = L + l_cnt0; x.cnt[1] = L + l_cnt1;
         x.map[0] = L + l_map0; x.map[1] = L + l_map1;
-        x.codes = L + l_codes;
+        x.ccode = L + l_ccode;
+        x.ctgt = (uint16_t *)(L + l_ctgt);
+        x.rown = (int32_t *)(L + l_rown);
         x.sel_p = (int32_t *)(L + l_selp); x.sel_j = (int32_t *)(L + l_selj); x.sel_ped = (int32_t *)(L + l_selped);
         x.rowc = (int32_t *)(L + l_rowc); x.rowpl = (int32_t *)(L + l_rowpl); x.rowpe = (int32_t *)(L + l_rowpe);
         x.rowmin = (int32_t *)(L + l_rowmin);
@@ -1061,6 +1064,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     if (myrank == 0) { // the home arrays (only rank 0's are read)
         CK(cudaMemsetAsync(B + o_hist, 0, 4 * 3 * 256, h->stream));
         CK(cudaMemsetAsync(B + o_ci, 0, 8 * (size_t)(n1 + 1), h->stream));
+        CK(cudaMemsetAsync(B + o_drop, 0, 4 * (size_t)(n1 + 1), h->stream));
         CK(cudaMemsetAsync(B + o_lo, 0x7f, 4 * (size_t)(n1 + 2), h->stream));
         CK(cudaMemsetAsync(B + o_hi, 0x80, 4 * (size_t)(n1 + 2), h->stream));
         CK(cudaMemsetAsync(B + o_best, 0xff, 8, h->stream));
@@ -1095,6 +1099,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.vstride = virt ? (int64_t)local_bytes : 0;
     a.hist = (int32_t *)(H + o_hist);
     a.ci = (int64_t *)(H + o_ci);
+    a.drop = (int32_t *)(H + o_drop);
     a.lo = (int32_t *)(H + o_lo);
     a.hi = (int32_t *)(H + o_hi);
     a.ctl = (int32_t *)(H + o_ctl); a.cte = (int32_t *)(H + o_cte);

@@ -143,7 +143,9 @@ struct LargeArgs {
         uint32_t *used[2];      // [Kl][W]   rows of the nodes of level L live in buffer L & 1
         void *cnt[2];           // [Kl][cs] CntT
         void *map[2];           // [Kl][n1s] MapT
-        uint8_t *codes;         // [Kl][cs]
+        uint8_t *ccode;         // [Kl][cs] candidate list of the row, in target order: rank codes
+        uint16_t *ctgt;         // [Kl][cs]                                          and targets
+        int32_t *rown;          // [Kl] entries in the row's candidate list
         int32_t *sel_p, *sel_j, *sel_ped; // nodes of the next level: parent row on its rank; target
                                           // (n2 = deletion, -1 = root; int16) | parent's rank << 16; PED
         int32_t *rowc;          // [Kl] per parent row: (codes < t) | (codes == t) << 16
@@ -157,6 +159,7 @@ struct LargeArgs {
     // home arrays (rank 0)
     int32_t *hist;          // [3][256] rotating global histograms
     int64_t *ci;            // [n1] candidates per level
+    int32_t *drop;          // [n1] nonzero: a valid child was left out of the candidate lists
     int32_t *lo, *hi;       // [n1 + 1] min / max survivor PED per level (init INT_MAX / INT_MIN)
     int32_t *ctl, *cte;     // [G * CTAs per rank] codes < t / == t per CTA
     unsigned long long *best;
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     __shared__ int s_cpre[2][LMAXGRID]; // exclusive prefix of the per-CTA counts
     __shared__ long long s_cnt;
     __shared__ int s_next; // A: next parent of this CTA's range (warps take parents dynamically)
+    __shared__ int s_drop; // A: a child of this CTA was left out of the candidate lists
     __shared__ LargeArgs::Rank s_rk[FG_MAXG]; // the ranks' array pointers (a.rk), dynamically indexed
     cg::grid_group grid = cg::this_grid();
     using C4 = Cnt4<CntT>;
@@ -394,6 +398,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         const int wcur = (i + EPW - 1) / EPW;                   // ... of a level-i row (entries 0..i-1)
         int base = lo, below = 0;
         bool first = true, keepall = false;
+        // candidate lists hold every valid child while the frontier is below K (all may survive), else only
+        // the children whose code can be selected (<= capc); a level that keeps everything although
+        // children were left out is redone with complete lists (rare: N == K and one child per parent)
+        bool listall = N < K;
         int tcode = 0, rq = 0;
         block_sync(); // P_i staged
 
@@ -401,8 +409,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
             // (each of the N parents has a deletion child <= U_i): their codes skip the histogram.
             const int capc = (N >= K) ? max(0, min(win, hi + pedDel - base + 1)) : win;
+            const uint32_t capc1 = (uint32_t)(capc + 1) * 0x01010101u; // (capc + 1 <= win + 1 <= 254)
             for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
-            if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; }
+            if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; s_drop = 0; }
             if (home0())
                 for (int k = threadIdx.x; k < 256; k += LNT) a.hist[((ps + 1) % 3) * 256 + k] = 0;
             block_sync();
@@ -513,10 +522,14 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     __syncwarp();
                     const int pb = pedp - base + 1 + edd;
                     const int cdel = rank_code(pedp + pedDel, base, win);
-                    uint8_t *crow = ML(codes) + (int64_t)k * cs;
+                    uint8_t *crow = ML(ccode) + (int64_t)k * cs;
+                    uint16_t *trow = ML(ctgt) + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
                     CntT *qc = Qcnt + (int64_t)k * cs;
-                    uint32_t rmin = 255u;
+                    uint32_t rmin2 = 0x00ff00ffu; // smallest code of the row, two 16-bit lanes
+                    int nsel = 0;              // entries of the row's list so far (warp-uniform)
+                    const unsigned lml = lanemask_lt();
+                    bool dropped = false;
                     for (int s = 0; s < S; ++s) {
                         const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
                         typename C4::V cv = C4::load(cr, u0);
@@ -542,6 +555,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                                 cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
                             }
                         }
+                        // the four slots' rank codes as bytes of one word (CODE_INVALID: used / past n2)
                         uint32_t word = 0;
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
@@ -550,17 +564,41 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             // used / out-of-range slots are selected in
                             const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
                                           (LAB ? c.esub * ms[b] : 0);
-                            int code = min(max(x, 0), win + 1);
-                            code = (u == n2) ? cdel : code; // deletion child (reading C5)
-                            code = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : code;
-                            if ((unsigned)(code - 1) < (unsigned)capc) atomicAdd(&s_hist[code * 32 + lane], 1);
-                            word |= (uint32_t)code << (8 * b);
-                            rmin = min(rmin, (uint32_t)code);
+                            int cd = min(max(x, 0), win + 1);
+                            cd = (u == n2) ? cdel : cd; // deletion child (reading C5)
+                            cd = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : cd;
+                            word |= (uint32_t)cd << (8 * b);
                         }
-                        *reinterpret_cast<uint32_t *>(crow + u0) = word;
+                        // histogram of the codes that can be selected (1..capc), per lane column
+                        uint32_t hmk = bytes_lt(word, capc1) & ~bytes_eq(word, 0u);
+                        while (hmk) {
+                            const int by = (__ffs(hmk) - 1) >> 3;
+                            hmk &= hmk - 1;
+                            atomicAdd(&s_hist[((word >> (8 * by)) & 0xffu) * 32 + lane], 1);
+                        }
+                        rmin2 = __vminu2(rmin2, __vminu2(word & 0x00ff00ffu, (word >> 8) & 0x00ff00ffu));
+                        const uint32_t validb = ~bytes_eq(word, 0xffffffffu) & 0x80808080u;
+                        const uint32_t listedb = listall ? validb : bytes_lt(word, capc1); // (255 > capc: never listed)
+                        dropped |= (validb & ~listedb) != 0u;
+                        unsigned bal[4];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) bal[b] = __ballot_sync(FULL, (listedb >> (8 * b + 7)) & 1u);
+                        // list entries in target order (u = 128 s + 4 lane + b: lanes first, then b)
+                        int pos = nsel + __popc(bal[0] & lml) + __popc(bal[1] & lml) + __popc(bal[2] & lml) + __popc(bal[3] & lml);
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if ((bal[b] >> lane) & 1u) {
+                                crow[pos] = (uint8_t)(word >> (8 * b));
+                                trow[pos++] = (uint16_t)(u0 + b);
+                            }
+                        nsel += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
                     }
-                    rmin = __reduce_min_sync(FULL, rmin);
-                    if (lane == 0) ML(rowmin)[k] = (int)rmin;
+                    const uint32_t rmin = __reduce_min_sync(FULL, min(rmin2 & 0xffffu, rmin2 >> 16));
+                    if (lane == 0) {
+                        ML(rowmin)[k] = (int)rmin;
+                        ML(rown)[k] = nsel;
+                    }
+                    if (dropped) s_drop = 1; // (benign race: every writer stores 1)
                     wcount += n2 - nused + 1;
                     __syncwarp();
                 }
@@ -576,12 +614,14 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 if (v) atomicAdd(&gh[bin], v);
             }
             if (first && threadIdx.x == 0) atomicAdd((unsigned long long *)&a.ci[i], (unsigned long long)s_cnt);
+            if (threadIdx.x == 0 && s_drop) a.drop[i] = 1;
             if (!xsync()) return;
             tick(0);
             // T: every CTA derives the same threshold from the global histogram
             const int64_t ci = a.ci[i];
             keepall = (ci <= K);
-            bool retry = false;
+            bool retry = false, slide = false;
+            if (keepall && !listall && a.drop[i]) { listall = true; retry = true; }
             if (!keepall) {
                 if (wib == 0) {
                     int hv[8], sum = 0;
@@ -619,63 +659,41 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 block_sync();
                 tcode = s_pre[0];
                 if (tcode) rq = s_pre[1];
-                else { retry = true; below += s_pre[1]; }
+                else { retry = slide = true; below += s_pre[1]; }
                 block_sync();
             }
             if (first) children += ci;
             ps++;
             first = false;
             if (!retry) break;
-            base += win; // the K-th smallest PED lies beyond the window: slide it (codes 0 = kept)
+            if (slide) base += win; // the K-th smallest PED lies beyond the window: slide it (codes 0 = kept)
         }
 
-        // ---------------- B: per-row counts of codes < t and == t (warp per row, static ranges) ----------------
-        const int vpr = cs / 16; // 16-byte code vectors per parent row
+        // ---------------- B: per-row counts of list codes < t and == t (lane per row, static ranges) ----------------
         const uint32_t t4 = (uint32_t)tcode * 0x01010101u;
-        const uint32_t inv4 = (uint32_t)CODE_INVALID * 0x01010101u;
-        const uint4 inv = make_uint4(inv4, inv4, inv4, inv4);
-        auto masks = [&](uint32_t v, uint32_t &mlt, uint32_t &meq) {
-            if (keepall) { mlt = ~bytes_eq(v, inv4) & 0x80808080u; meq = 0u; }
-            else { mlt = bytes_lt(v, t4); meq = bytes_eq(v, t4); }
-        };
-        auto rowvec = [&](int k, int x) { return reinterpret_cast<const uint4 *>(ML(codes) + (int64_t)k * cs)[x]; };
         {
             int wl = 0, we = 0;
-            // 32 rows per step, one per lane; only rows whose smallest code can be selected are read
-            // (up to 8 of them with their loads in flight together)
-            constexpr int BR = FG_LBR;
+            // 32 rows per step, one per lane; only rows whose smallest code can be selected are read (SWAR
+            // byte compares over 16-byte vectors of the list's codes, bytes past the list masked off)
             for (int k0 = p0; k0 < p1; k0 += 32) {
                 const int kl = k0 + lane;
-                const bool q = kl < p1 && (keepall || ML(rowmin)[kl] <= tcode);
-                unsigned qm = __ballot_sync(FULL, q);
                 int myl = 0, mye = 0; // counts of row kl
-                while (qm) {
-                    int zr[BR];
+                if (kl < p1 && (keepall || ML(rowmin)[kl] <= tcode)) {
+                    const int n = ML(rown)[kl];
+                    const uint4 *cv = reinterpret_cast<const uint4 *>(ML(ccode) + (int64_t)kl * cs);
+                    for (int x = 0; 16 * x < n; ++x) {
+                        const uint4 v = cv[x];
+                        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int r = 0; r < BR; ++r) {
-                        zr[r] = qm ? __ffs(qm) - 1 : -1;
-                        if (qm) qm &= qm - 1;
-                    }
-                    int lt[BR], eq[BR];
-#pragma unroll
-                    for (int r = 0; r < BR; ++r) { lt[r] = 0; eq[r] = 0; }
-                    for (int x = lane; x < vpr; x += 32) {
-                        uint4 v[BR];
-#pragma unroll
-                        for (int r = 0; r < BR; ++r) v[r] = zr[r] >= 0 ? rowvec(k0 + zr[r], x) : inv;
-#pragma unroll
-                        for (int r = 0; r < BR; ++r) {
-                            uint32_t m0, e0;
-                            masks(v[r].x, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                            masks(v[r].y, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                            masks(v[r].z, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
-                            masks(v[r].w, m0, e0); lt[r] += __popc(m0); eq[r] += __popc(e0);
+                        for (int w = 0; w < 4; ++w) {
+                            const int nbv = min(max(n - 16 * x - 4 * w, 0), 4); // list bytes in this word
+                            const uint32_t vm = nbv == 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nbv)) - 1u));
+                            if (keepall) myl += __popc(vm);
+                            else {
+                                myl += __popc(bytes_lt(wv[w], t4) & vm);
+                                mye += __popc(bytes_eq(wv[w], t4) & vm);
+                            }
                         }
-                    }
-#pragma unroll
-                    for (int r = 0; r < BR; ++r) {
-                        const int l = __reduce_add_sync(FULL, lt[r]), e = __reduce_add_sync(FULL, eq[r]);
-                        if (lane == zr[r]) { myl = l; mye = e; }
                     }
                 }
                 int il = myl, ie = mye;
@@ -734,9 +752,27 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         // B owner + the owner CTA's warps before the owner warp + the owner's rows before it.
         {
             int mylo = 0x7fffffff, myhi = (int)0x80000000;
+            const unsigned lml = lanemask_lt();
+            auto is_lt = [&](uint32_t e, bool in) { return keepall ? in : (int)(e & 0xffu) < tcode; };
+            // survivor (row k, target u, rank code) at global position pos of the next level
+            auto emit = [&](int k, int u, int code, int pos) {
+                int ped;
+                if (code >= 1 && code <= win) ped = base + code - 1;
+                else // below the window or saturated: recompute from the parent's materialised row (rare)
+                    ped = large_child_scalar<MapT, CntT, LAB>(a, d, s_pq, s_pl, ML(ped[cu])[k], Qcnt + (int64_t)k * cs,
+                                                              Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
+                // its descriptor goes to its owner (a peer when sharded); the parent is row k of this rank
+                const int no = rowner(pos, Nn);
+                const int np = pos - rstart(Nn, no);
+                RK(no, sel_p)[np] = k;
+                RK(no, sel_j)[np] = u | (RANK << 16);
+                RK(no, sel_ped)[np] = ped;
+                mylo = min(mylo, ped);
+                myhi = max(myhi, ped);
+            };
+            auto is_eq = [&](uint32_t e) { return !keepall && (int)(e & 0xffu) == tcode; };
             // 32 rows per batch (row kb + l GW for lane l): their counts and prefixes are loaded in parallel,
-            // then the rows holding survivors are expanded one after the other, the next one's first code
-            // vector already in flight (the loop is otherwise a chain of dependent global round trips)
+            // then the rows holding survivors are expanded one after the other (lane x: entry x of the list)
             for (int kb = gw; kb < Nl; kb += 32 * GW) {
                 const int kl = kb + lane * GW;
                 int rc = 0, lp = 0, ep = 0;
@@ -761,74 +797,66 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                 }
 #endif
-                int zn = hm ? __ffs(hm) - 1 : 0;
-                uint4 vn = (hm && lane < vpr) ? rowvec(kb + zn * GW, lane) : inv;
-                while (hm) {
-                const int z = zn;
-                hm &= hm - 1;
-                const int k = kb + z * GW;
-                const uint4 v0 = vn;
-                if (hm) { zn = __ffs(hm) - 1; vn = lane < vpr ? rowvec(kb + zn * GW, lane) : inv; }
-                const int ltpre = __shfl_sync(FULL, lp, z), eqpre = __shfl_sync(FULL, ep, z);
-                int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
-                for (int xb = 0; xb < vpr; xb += 32) {
-                    const int x = xb + lane;
-                    const uint4 v = xb == 0 ? v0 : (x < vpr ? rowvec(k, x) : inv);
-                    uint32_t ml[4], mq[4];
-                    masks(v.x, ml[0], mq[0]); masks(v.y, ml[1], mq[1]);
-                    masks(v.z, ml[2], mq[2]); masks(v.w, ml[3], mq[3]);
-                    const int nlt = __popc(ml[0]) + __popc(ml[1]) + __popc(ml[2]) + __popc(ml[3]);
-                    const int neq = __popc(mq[0]) + __popc(mq[1]) + __popc(mq[2]) + __popc(mq[3]);
-                    if (!__any_sync(FULL, (nlt | neq) != 0)) continue;
-                    int einc = neq;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(FULL, einc, o);
-                        if (lane >= o) einc += y;
-                    }
-                    const int adm = min(neq, max(0, rq - (eq_seen + einc - neq))); // ties admitted in code order
-                    const int keep = nlt + adm;
-                    int kinc = keep;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(FULL, kinc, o);
-                        if (lane >= o) kinc += y;
-                    }
-                    if (keep) {
-                        int pos = out + kinc - keep, ecnt = 0;
-                        const int ub = 16 * x;
-                        const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+                const int rn = has ? ML(rown)[kl] : 0;
+                // rows with few survivors: lane per row (32 rows in flight); the rest: warp per row below
+                const int nkeep = keepall ? (rc & 0xffff) : (rc & 0xffff) + min(rc >> 16, max(0, rq - ep));
+                const bool light = has && nkeep <= 8;
+                hm &= ~__ballot_sync(FULL, light);
+                if (light) {
+                    int out = lp + (keepall ? 0 : min(rq, ep)), eq_seen = ep, left = nkeep;
+                    const uint4 *cv = reinterpret_cast<const uint4 *>(ML(ccode) + (int64_t)kl * cs);
+                    for (int x = 0; left > 0 && 16 * x < rn; ++x) {
+                        const uint4 v = cv[x];
+                        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                         for (int w = 0; w < 4; ++w) {
-                            uint32_t m = ml[w], e = mq[w];
-                            while (e && ecnt < adm) { const uint32_t lowb = e & (0u - e); m |= lowb; e ^= lowb; ++ecnt; }
-                            while (m) {
-                                const int by = (__ffs(m) - 1) >> 3;
-                                m &= m - 1;
-                                const int u = ub + 4 * w + by;
-                                const int code = (int)((words[w] >> (8 * by)) & 0xffu);
-                                int ped;
-                                if (code >= 1 && code <= win) ped = base + code - 1;
-                                else // saturated code: recompute from the parent's materialised row (rare)
-                                    ped = large_child_scalar<MapT, CntT, LAB>(
-                                        a, d, s_pq, s_pl, ML(ped[cu])[k], Qcnt + (int64_t)k * cs,
-                                        Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
-                                // the node of level i+1 at global position pos: its descriptor goes to its
-                                // owner (a peer when sharded); the parent is row k of this rank
-                                const int no = rowner(pos, Nn);
-                                const int np = pos - rstart(Nn, no);
-                                RK(no, sel_p)[np] = k;
-                                RK(no, sel_j)[np] = u | (RANK << 16);
-                                RK(no, sel_ped)[np] = ped;
-                                mylo = min(mylo, ped);
-                                myhi = max(myhi, ped);
-                                ++pos;
+                            const int nbv = min(max(rn - 16 * x - 4 * w, 0), 4);
+                            const uint32_t vm = nbv == 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nbv)) - 1u));
+                            uint32_t ml = keepall ? vm : (bytes_lt(wv[w], t4) & vm);
+                            uint32_t mq = keepall ? 0u : (bytes_eq(wv[w], t4) & vm);
+                            // ties at t are admitted in list (= target) order up to the quota rq
+                            const int nq = __popc(mq);
+                            for (int z = min(nq, max(0, rq - eq_seen)); z > 0; --z) { const uint32_t low = mq & (0u - mq); ml |= low; mq ^= low; }
+                            eq_seen += nq;
+                            while (ml) {
+                                const int by = (__ffs(ml) - 1) >> 3;
+                                ml &= ml - 1;
+                                const int idx = 16 * x + 4 * w + by;
+                                emit(kl, (int)ML(ctgt)[(int64_t)kl * cs + idx], (int)((wv[w] >> (8 * by)) & 0xffu), out++);
+                                --left;
                             }
                         }
                     }
-                    out += __shfl_sync(FULL, kinc, 31);
-                    eq_seen += __shfl_sync(FULL, einc, 31);
                 }
+                while (hm) {
+                    const int z = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const int k = kb + z * GW;
+                    const int n = __shfl_sync(FULL, rn, z);
+                    const int ltpre = __shfl_sync(FULL, lp, z), eqpre = __shfl_sync(FULL, ep, z);
+                    int eq_seen = eqpre, out = ltpre + (keepall ? 0 : min(rq, eqpre));
+                    auto ent = [&](int x) -> uint32_t { // code | target << 8 of list entry x; padding: code 255
+                        return x < n ? (uint32_t)ML(ccode)[(int64_t)k * cs + x] | ((uint32_t)ML(ctgt)[(int64_t)k * cs + x] << 8)
+                                     : 0xffffffffu;
+                    };
+                    uint32_t en = ent(lane);
+                    for (int xb = 0; xb < n; xb += 32) {
+                        const int x = xb + lane;
+                        const uint32_t e = en;
+                        if (xb + 32 < n) en = ent(x + 32);
+                        const bool lt = is_lt(e, x < n), eq = is_eq(e);
+                        // ties at t are admitted in list (= target) order up to the quota rq
+                        const unsigned eb = __ballot_sync(FULL, eq);
+                        const bool keep = lt || (eq && eq_seen + __popc(eb & lml) < rq);
+                        const unsigned kbm = __ballot_sync(FULL, keep);
+                        if (keep) {
+                            const int pos = out + __popc(kbm & lml);
+                            const int u = (int)(e >> 8), code = (int)(e & 0xffu);
+                            emit(k, u, code, pos);
+                        }
+                        out += __popc(kbm);
+                        eq_seen += __popc(eb);
+                    }
                 }
             }
             mylo = __reduce_min_sync(FULL, mylo);
