@@ -462,7 +462,7 @@ def run_pair(args, rank, local_rank, world):
             "unit": "GB/s", "frac": (ach / hbm_peak) if ach else None, "traffic": traffic,
             "alg_bytes_per_launch": st["alg_bytes"],
             "note": "algorithmic bytes = SURVEY §8(d) D.4 per level (parent PED + lambda rows read, child rows written); "
-                    "traffic = ncu dram read+write of the same launch (counters, used masks and rank codes on top)"}
+                    "traffic = ncu dram read+write of the same launch (counters, used masks and candidate lists on top)"}
     return {
         "metric": METRIC, "value": args.steps / (dev_ms / 1e3), "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
