@@ -60,6 +60,14 @@ extern "C" {
                                          C10 of Alg. 1); never a higher cost than the
                                          paper-literal rule.  Batched path only (n2 <= 128): a pair that needs
                                          the whole-GPU or sharded path fails with FASTGED_ERR_ARG. */
+/* method variant ("approximate top-k selection may become an option"
+ * for extreme K): each level keeps the min(K, c_i) smallest children under the coarse key
+ * (floor((PED - lo_i) / 2^shift), parent, child), lo_i = the smallest PED of the level's parents --
+ * children in one PED bin are ranked by position only.  shift = 1..15 (0 = the exact selection).  Runs on
+ * the whole-GPU kernel (every pair of a batch is routed there); levels_out[3i+2] then reports the K-th
+ * smallest key's bin. */
+#define FASTGED_FLAG_APPROX(shift) ((uint32_t)((shift) & 15) << 8)
+#define FASTGED_FLAG_APPROX_MASK (15u << 8)
 
 /* Limits of this build (exceeding one returns FASTGED_ERR_CAPACITY, never a silent change). */
 #define FASTGED_MAX_N 65534        /* vertices of a source graph g1                               */

@@ -209,6 +209,11 @@ static int64_t mapping_cost(const og_graph *g1, const og_graph *g2, const og_cos
 }
 
 #define OG_LAST_BY_TOTAL 1 /* method variant: last level ranked by PED + completion */
+/* method variant ("approximate top-k selection"): flags bits 8..11 = s > 0 --
+ * each level keeps the min(K, c_i) smallest children under the coarse key (floor((PED - lo_i) / 2^s), p, j),
+ * lo_i = the smallest PED of the level's parents: children whose PEDs share a bin of width 2^s are
+ * ranked by position only (s = 0: the exact selection) */
+#define OG_APPROX_SHIFT(flags) (((flags) >> 8) & 15)
 
 /*
  * og_kbest: Algorithm 1 with the readings listed at the top.
@@ -249,6 +254,10 @@ int og_kbest_ex(const og_graph *g1, const og_graph *g2, const og_costs *c, int64
     for (int i = 0; i < n1 && rc == OG_OK; i++) { /* ForEach v in V1, order C4 */
         /* Branch + evaluate every node of List. */
         int64_t C = N * (int64_t)(n2 + 1);
+        const int shift = OG_APPROX_SHIFT(flags);
+        int64_t lo = ped[0]; /* smallest parent PED (the bins' origin) */
+        for (int64_t p = 1; p < N; p++)
+            if (ped[p] < lo) lo = ped[p];
         cand *pool = (cand *)malloc(sizeof(cand) * (size_t)C);
         char *valid = (char *)malloc((size_t)C);
         if (!pool || !valid) { free(pool); free(valid); rc = OG_ERR_MEM; break; }
@@ -265,7 +274,7 @@ int og_kbest_ex(const og_graph *g1, const og_graph *g2, const og_costs *c, int64
                 pool[slot].ped = e;
                 pool[slot].p = p;
                 pool[slot].j = j;
-                pool[slot].key = e;
+                pool[slot].key = shift ? (e - lo) >> shift : e; /* (e >= ped[p] >= lo) */
             }
         }
         int64_t cnt = 0;

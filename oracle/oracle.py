@@ -106,6 +106,11 @@ def _costs(c):
 LAST_BY_TOTAL = 1  # method variant: last level ranked by PED + completion
 
 
+def APPROX(shift: int) -> int:
+    """flags of the approximate top-K variant: bins of 2**shift PED units."""
+    return (int(shift) & 15) << 8
+
+
 def kbest(g1, g2, costs, K, levels: bool = False, flags: int = 0):
     """Returns dict(cost, mapping, children, parents[, levels])."""
     keep = []

@@ -22,6 +22,11 @@ FLAG_FORCE_LARGE = 4
 FLAG_VIRTUAL_SHARDS = 8
 FLAG_LAST_BY_TOTAL = 16  # method variant: last level ranked by PED + completion (batched path only)
 
+
+def FLAG_APPROX(shift: int) -> int:
+    """Method variant: approximate top-K with PED bins of 2**shift (include/fastged.h FASTGED_FLAG_APPROX)."""
+    return (int(shift) & 15) << 8
+
 # The symbols include/fastged.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "fastged_create", "fastged_destroy", "fastged_last_error", "fastged_solve_pair", "fastged_solve_pair_ex",

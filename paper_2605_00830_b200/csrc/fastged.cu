@@ -613,7 +613,8 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
                         ((int64_t)d.m1 + d.m2) * std::max(c->esub, std::max(c->edel, c->eins)) + 512;
         if (bound >= ((int64_t)1 << 31))
             fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
-        if (fits_batched(d.n1, d.n2, k, d.labelled ? d.nlab : 0) && !(h->flags & FASTGED_FLAG_FORCE_LARGE))
+        if (fits_batched(d.n1, d.n2, k, d.labelled ? d.nlab : 0) && !(h->flags & FASTGED_FLAG_FORCE_LARGE) &&
+            !(h->flags & FASTGED_FLAG_APPROX_MASK))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
             b->large.push_back(p); // solved by the whole-GPU kernel after the batched launches
@@ -1077,6 +1078,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.c = fg::Costs{c->vsub, c->vdel, c->vins, c->esub, c->edel, c->eins};
     a.K = Kc;
     a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
+    a.ashift = (int32_t)((h->flags & FASTGED_FLAG_APPROX_MASK) >> 8);
     a.W = W;
     a.cs = cs;
     a.S = cs / 128;
@@ -1412,7 +1414,7 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
             return FASTGED_OK;
         }
         if (!fits_batched(g1->n, g2->n, k, labelled_pair(g1, g2) ? g2_label_count(g2) : 0) ||
-            (h->flags & FASTGED_FLAG_FORCE_LARGE)) {
+            (h->flags & (FASTGED_FLAG_FORCE_LARGE | FASTGED_FLAG_APPROX_MASK))) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }

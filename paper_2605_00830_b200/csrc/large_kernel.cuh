@@ -39,6 +39,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "batch_kernel.cuh"
 
@@ -118,6 +119,7 @@ struct LargeArgs {
     PairDesc pd;
     Costs c;
     int32_t K, win, W;
+    int32_t ashift;         // method variant (NEXT-4): approximate top-K with PED bins of 2^ashift (0 = exact)
     int32_t cs, S;          // row stride of codes / counters (multiple of 128 >= n2 + 1); S = cs / 128
     int32_t n1s;            // lambda row stride in elements (4-byte multiple)
     int32_t n1r;            // staged P_i list capacity in shared memory (>= max d, multiple of 4)
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         for (;;) { // ---------------- A + T ----------------
             // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
             // (each of the N parents has a deletion child <= U_i): their codes skip the histogram.
-            const int capc = (N >= K) ? max(0, min(win, hi + pedDel - base + 1)) : win;
+            const int capc = (N >= K) ? max(0, min(win, ((hi + pedDel - base) >> a.ashift) + 1)) : win;
             const uint32_t capc1 = (uint32_t)(capc + 1) * 0x01010101u; // (capc + 1 <= win + 1 <= 254)
             for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
             if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; s_drop = 0; }
@@ -521,7 +523,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     }
                     __syncwarp();
                     const int pb = pedp - base + 1 + edd;
-                    const int cdel = rank_code(pedp + pedDel, base, win);
+                    const int xdel = pedp + pedDel - base + 1;
+                    const int cdel = a.ashift ? (xdel <= 0 ? 0 : min(((xdel - 1) >> a.ashift) + 1, win + 1)) : rank_code(pedp + pedDel, base, win);
                     uint8_t *crow = ML(ccode) + (int64_t)k * cs;
                     uint16_t *trow = ML(ctgt) + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
@@ -530,69 +533,76 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     int nsel = 0;              // entries of the row's list so far (warp-uniform)
                     const unsigned lml = lanemask_lt();
                     bool dropped = false;
-                    for (int s = 0; s < S; ++s) {
-                        const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
-                        typename C4::V cv = C4::load(cr, u0);
-                        if (jn >= 0 && wu < W) cv = C4::add_bits(cv, (adjw(jn, wu) >> (u0 & 31)) & 0xfu);
-                        if (first) C4::store(qc, u0, cv);
-                        const uint32_t ub = (sU[min(wu, 31)] >> (u0 & 31)) & 0xfu;
-                        const uint32_t mnib = (uint32_t)(mm >> (4 * s)) & 0xfu;
-                        int cb[4] = {0, 0, 0, 0}, ms[4] = {0, 0, 0, 0};
-                        if (scatter) {
-                            int4 *dp = reinterpret_cast<int4 *>(D + u0);
-                            const int4 dv = *dp;
-                            *dp = make_int4(0, 0, 0, 0);
-                            cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
-                            if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
-                        } else {
-                            uint32_t m = nzb;
-                            while (m) {
-                                const int w = __ffs(m) - 1;
-                                m &= m - 1;
-                                const uint4 av = *reinterpret_cast<const uint4 *>(adjT + (int64_t)w * cs + u0);
-                                const uint32_t bw = sB[w];
-                                cb[0] += __popc(av.x & bw); cb[1] += __popc(av.y & bw);
-                                cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
+                    // the row's slots, 4 per lane per step (two instantiations: exact / approximate codes)
+                    auto slots = [&](auto apx) {
+                        constexpr bool APX = decltype(apx)::value;
+                        for (int s = 0; s < S; ++s) {
+                            const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
+                            typename C4::V cv = C4::load(cr, u0);
+                            if (jn >= 0 && wu < W) cv = C4::add_bits(cv, (adjw(jn, wu) >> (u0 & 31)) & 0xfu);
+                            if (first) C4::store(qc, u0, cv);
+                            const uint32_t ub = (sU[min(wu, 31)] >> (u0 & 31)) & 0xfu;
+                            const uint32_t mnib = (uint32_t)(mm >> (4 * s)) & 0xfu;
+                            int cb[4] = {0, 0, 0, 0}, ms[4] = {0, 0, 0, 0};
+                            if (scatter) {
+                                int4 *dp = reinterpret_cast<int4 *>(D + u0);
+                                const int4 dv = *dp;
+                                *dp = make_int4(0, 0, 0, 0);
+                                cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
+                                if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
+                            } else {
+                                uint32_t m = nzb;
+                                while (m) {
+                                    const int w = __ffs(m) - 1;
+                                    m &= m - 1;
+                                    const uint4 av = *reinterpret_cast<const uint4 *>(adjT + (int64_t)w * cs + u0);
+                                    const uint32_t bw = sB[w];
+                                    cb[0] += __popc(av.x & bw); cb[1] += __popc(av.y & bw);
+                                    cb[2] += __popc(av.z & bw); cb[3] += __popc(av.w & bw);
+                                }
                             }
-                        }
-                        // the four slots' rank codes as bytes of one word (CODE_INVALID: used / past n2)
-                        uint32_t word = 0;
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            const int u = u0 + b;
-                            // branch-free: every slot's value is computed, then the deletion slot and the
-                            // used / out-of-range slots are selected in
-                            const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
-                                          (LAB ? c.esub * ms[b] : 0);
-                            int cd = min(max(x, 0), win + 1);
-                            cd = (u == n2) ? cdel : cd; // deletion child (reading C5)
-                            cd = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : cd;
-                            word |= (uint32_t)cd << (8 * b);
-                        }
-                        // histogram of the codes that can be selected (1..capc), per lane column
-                        uint32_t hmk = bytes_lt(word, capc1) & ~bytes_eq(word, 0u);
-                        while (hmk) {
-                            const int by = (__ffs(hmk) - 1) >> 3;
-                            hmk &= hmk - 1;
-                            atomicAdd(&s_hist[((word >> (8 * by)) & 0xffu) * 32 + lane], 1);
-                        }
-                        rmin2 = __vminu2(rmin2, __vminu2(word & 0x00ff00ffu, (word >> 8) & 0x00ff00ffu));
-                        const uint32_t validb = ~bytes_eq(word, 0xffffffffu) & 0x80808080u;
-                        const uint32_t listedb = listall ? validb : bytes_lt(word, capc1); // (255 > capc: never listed)
-                        dropped |= (validb & ~listedb) != 0u;
-                        unsigned bal[4];
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) bal[b] = __ballot_sync(FULL, (listedb >> (8 * b + 7)) & 1u);
-                        // list entries in target order (u = 128 s + 4 lane + b: lanes first, then b)
-                        int pos = nsel + __popc(bal[0] & lml) + __popc(bal[1] & lml) + __popc(bal[2] & lml) + __popc(bal[3] & lml);
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-                            if ((bal[b] >> lane) & 1u) {
-                                crow[pos] = (uint8_t)(word >> (8 * b));
-                                trow[pos++] = (uint16_t)(u0 + b);
+                            // the four slots' rank codes as bytes of one word (CODE_INVALID: used / past n2)
+                            uint32_t word = 0;
+    #pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const int u = u0 + b;
+                                // branch-free: every slot's value is computed, then the deletion slot and the
+                                // used / out-of-range slots are selected in
+                                const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
+                                              (LAB ? c.esub * ms[b] : 0);
+                                // rank code: x = PED - base + 1; approximate variant: PED bins of 2^ashift
+                                int cd = APX ? (x <= 0 ? 0 : min(((x - 1) >> a.ashift) + 1, win + 1)) : min(max(x, 0), win + 1);
+                                cd = (u == n2) ? cdel : cd; // deletion child (reading C5)
+                                cd = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : cd;
+                                word |= (uint32_t)cd << (8 * b);
                             }
-                        nsel += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
-                    }
+                            // histogram of the codes that can be selected (1..capc), per lane column
+                            uint32_t hmk = bytes_lt(word, capc1) & ~bytes_eq(word, 0u);
+                            while (hmk) {
+                                const int by = (__ffs(hmk) - 1) >> 3;
+                                hmk &= hmk - 1;
+                                atomicAdd(&s_hist[((word >> (8 * by)) & 0xffu) * 32 + lane], 1);
+                            }
+                            rmin2 = __vminu2(rmin2, __vminu2(word & 0x00ff00ffu, (word >> 8) & 0x00ff00ffu));
+                            const uint32_t validb = ~bytes_eq(word, 0xffffffffu) & 0x80808080u;
+                            const uint32_t listedb = listall ? validb : bytes_lt(word, capc1); // (255 > capc: never listed)
+                            dropped |= (validb & ~listedb) != 0u;
+                            unsigned bal[4];
+    #pragma unroll
+                            for (int b = 0; b < 4; ++b) bal[b] = __ballot_sync(FULL, (listedb >> (8 * b + 7)) & 1u);
+                            // list entries in target order (u = 128 s + 4 lane + b: lanes first, then b)
+                            int pos = nsel + __popc(bal[0] & lml) + __popc(bal[1] & lml) + __popc(bal[2] & lml) + __popc(bal[3] & lml);
+    #pragma unroll
+                            for (int b = 0; b < 4; ++b)
+                                if ((bal[b] >> lane) & 1u) {
+                                    crow[pos] = (uint8_t)(word >> (8 * b));
+                                    trow[pos++] = (uint16_t)(u0 + b);
+                                }
+                            nsel += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
+                        }
+                    };
+                    if (a.ashift) slots(std::true_type{});
+                    else slots(std::false_type{});
                     const uint32_t rmin = __reduce_min_sync(FULL, min(rmin2 & 0xffffu, rmin2 >> 16));
                     if (lane == 0) {
                         ML(rowmin)[k] = (int)rmin;
@@ -666,7 +676,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             ps++;
             first = false;
             if (!retry) break;
-            if (slide) base += win; // the K-th smallest PED lies beyond the window: slide it (codes 0 = kept)
+            if (slide) base += win << a.ashift; // the K-th smallest lies beyond the window: slide it (codes 0 = kept)
         }
 
         // ---------------- B: per-row counts of list codes < t and == t (lane per row, static ranges) ----------------
@@ -757,8 +767,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             // survivor (row k, target u, rank code) at global position pos of the next level
             auto emit = [&](int k, int u, int code, int pos) {
                 int ped;
-                if (code >= 1 && code <= win) ped = base + code - 1;
-                else // below the window or saturated: recompute from the parent's materialised row (rare)
+                if (a.ashift == 0 && code >= 1 && code <= win) ped = base + code - 1;
+                else // below the window, saturated or a PED bin: recompute from the parent's materialised row
                     ped = large_child_scalar<MapT, CntT, LAB>(a, d, s_pq, s_pl, ML(ped[cu])[k], Qcnt + (int64_t)k * cs,
                                                               Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
                 // its descriptor goes to its owner (a peer when sharded); the parent is row k of this rank
@@ -869,7 +879,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         if (home0() && threadIdx.x == 0 && a.levels_out) {
             a.levels_out[3 * i] = N;
             a.levels_out[3 * i + 1] = a.ci[i];
-            a.levels_out[3 * i + 2] = keepall ? -1 : (int64_t)(base + tcode - 1);
+            // the K-th smallest key: its PED (exact) or its bin above the level's smallest parent PED (approximate)
+            a.levels_out[3 * i + 2] = keepall ? -1 : (a.ashift ? (int64_t)(((base - lo) >> a.ashift) + tcode - 1) : (int64_t)(base + tcode - 1));
         }
         parents += N;
         algb += (int64_t)N * (4 + ESZ * d) + (int64_t)Nn * (ESZ * (2 * i + 1) + 8);

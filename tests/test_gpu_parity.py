@@ -211,6 +211,40 @@ def test_per_level_trace(fg, oracle, flags):
 
 
 # ------------------------------------------------------------------ method variant (NEXT-4)
+@pytest.mark.parametrize("shift", [1, 3])
+@pytest.mark.parametrize("window", [0, 2], ids=["window253", "window2"])
+def test_variant_approx_topk_matches_oracle(fg, oracle, shift, window):
+    """FASTGED_FLAG_APPROX (approximate top-K: PED bins of 2^shift) on the whole-GPU kernel against the
+    oracle's variant, bit-exact: cost, mapping, children and per-level records (the threshold is the K-th
+    smallest key's bin) for single pairs, a batch (every pair routed to the whole-GPU kernel) and 2 virtual
+    ranks of the sharded mode."""
+    flags = fg.FLAG_APPROX(shift) | (fg.FLAG_DEBUG_WINDOW if window else 0)
+    h = fg.Handle(0, flags=flags)
+    hs = fg.Handle(0, world_size=2, flags=flags | fg.FLAG_VIRTUAL_SHARDS)
+    rng = synth.rng_for(71, shift, window)
+    pairs = []
+    for k in range(8):
+        n1, n2 = int(rng.integers(3, 60)), int(rng.integers(3, 60))
+        pairs.append((synth.er_graph(rng, n1, (0.1, 0.3)[k % 2], 4, 1 + k % 2), synth.er_graph(rng, n2, (0.1, 0.3)[k % 2], 4, 1 + k % 2)))
+    for k, (g1, g2) in enumerate(pairs):
+        K = int(rng.integers(1, 2000))
+        o = oracle.kbest(g1, g2, COSTS["setting1"], K, levels=True, flags=oracle.APPROX(shift))
+        for hh in (h, hs):
+            r = hh.solve_pair(g1, g2, COSTS["setting1"], K, levels=True)
+            assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]), (k, K)
+            assert r["children"] == o["children"] and r["levels"] == [tuple(x) for x in o["levels"]], (k, K)
+    g1, g2 = synth.large_pair(300, 0.05, seed=12)
+    o = oracle.kbest(g1, g2, COSTS["setting1"], 3000, flags=oracle.APPROX(shift))
+    r = h.solve_pair(g1, g2, COSTS["setting1"], 3000)
+    assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"])
+    gc, gm, gch = gpu_batch(fg, h, pairs, COSTS["setting2"], 200)
+    oc, om, och = oracle.kbest_batch(pairs, COSTS["setting2"], 200, flags=oracle.APPROX(shift))
+    for k in range(len(pairs)):
+        assert gc[k] == oc[k] and np.array_equal(gm[k], om[k]) and gch[k] == och[k], k
+    h.close()
+    hs.close()
+
+
 @pytest.mark.parametrize("window", [0, 2], ids=["window127", "window2"])
 def test_variant_last_by_total_matches_oracle(fg, oracle, window):
     """FASTGED_FLAG_LAST_BY_TOTAL (last level ranked by PED + completion, the alternative to reading C10)

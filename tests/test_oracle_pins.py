@@ -317,3 +317,64 @@ def test_oracle_rejects_bad_input(oracle_lib):
         oracle_lib.kbest(g, g, COSTS["unit"], 0)
     with pytest.raises(OracleError):
         oracle_lib.kbest(g, g, (1, -1, 1, 1, 1, 1), 2)
+
+
+# ------------------------------------------------------------------ NEXT-4: approximate top-K
+def _lex_first_k(n1, n2, K):
+    """The lexicographically first K complete nodes of the vertex-branching tree in its canonical child
+    order (free targets ascending, deletion last; readings C5, C13), from the brute force's enumeration."""
+    from oracle import bruteforce
+    F = bruteforce.injections(n1, n2)
+    if n1 == 0:
+        return F
+    key = np.where(F == bruteforce.DEL, n2, F)
+    order = np.lexsort(key.T[::-1])  # column 0 most significant
+    return F[order[:K]]
+
+
+def test_approx_topk_one_bin_is_lexicographic_first_k(oracle_lib):
+    """With one bin for every PED (2^15 wide) the keys all tie, so every level keeps its first K children in
+    (p, j) order; the survivors are then the lexicographically first K complete mappings (each parent has a
+    deletion child, so the first K children of a level come from its first K parents), and the result is the
+    order-free cost minimum over them, first position on ties -- the brute force's enumeration and formula."""
+    from oracle import bruteforce
+    rng = synth.rng_for(5151)
+    differs = 0
+    for k in range(120):
+        n1, n2 = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        g1 = synth.er_graph(rng, n1, (0.2, 0.5, 0.8)[k % 3], 2, 1 + k % 2)
+        g2 = synth.er_graph(rng, n2, (0.2, 0.5, 0.8)[k % 3], 2, 1 + k % 2)
+        c = (COSTS["unit"], COSTS["setting1"], ASYM)[k % 3]
+        for K in (1, 3, 20):
+            first = _lex_first_k(n1, n2, K)
+            cst = bruteforce.costs_of(g1, g2, c, first)
+            b = int(np.argmin(cst))
+            r = oracle_lib.kbest(g1, g2, c, K, flags=oracle_lib.APPROX(15))
+            assert r["cost"] == int(cst[b]), (k, K)
+            assert r["mapping"].tolist() == first[b].tolist(), (k, K)
+            differs += r["cost"] != oracle_lib.kbest(g1, g2, c, K)["cost"]
+    assert differs > 0  # the pin separates the variant from the exact selection
+
+
+def test_approx_topk_bounds(oracle_lib):
+    """Any bin width: shift 0 is the exact selection; the cost is >= the exact GED, the witness re-verifies,
+    and once K covers every level's width (nothing is dropped) the cost is the exact GED."""
+    from oracle import bruteforce
+    rng = synth.rng_for(5252)
+    for k in range(100):
+        n1, n2 = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        g1 = synth.er_graph(rng, n1, (0.2, 0.5, 0.8)[k % 3], 3, 1 + k % 2)
+        g2 = synth.er_graph(rng, n2, (0.2, 0.5, 0.8)[k % 3], 3, 1 + k % 2)
+        c = (COSTS["unit"], COSTS["setting1"], ASYM)[k % 3]
+        ged = bruteforce.exact_ged(g1, g2, c)[0]
+        full = bruteforce.width(n1, n2, n1)
+        for K in (1, 4, full):
+            ex = oracle_lib.kbest(g1, g2, c, K)
+            z = oracle_lib.kbest(g1, g2, c, K, flags=oracle_lib.APPROX(0))
+            assert z["cost"] == ex["cost"] and z["mapping"].tolist() == ex["mapping"].tolist()
+            for s in (1, 2, 3):
+                r = oracle_lib.kbest(g1, g2, c, K, flags=oracle_lib.APPROX(s))
+                assert r["cost"] >= ged
+                assert oracle_lib.mapping_cost(g1, g2, c, r["mapping"]) == r["cost"]
+                if K >= full:
+                    assert r["cost"] == ged
