@@ -1094,6 +1094,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.adjT = (const uint32_t *)(dblob + o_adjT);
     a.G = G;
     a.nb = nb;
+    a.kl = (int32_t)Kl;
     a.rank = myrank;
     a.virt = virt ? 1 : 0;
     a.rk = (const fg::LargeArgs::Rank *)(B + o_rk);

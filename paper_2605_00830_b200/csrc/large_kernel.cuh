@@ -140,6 +140,7 @@ struct LargeArgs {
     // grid (one GPU; the exchange protocol is the same, only the barrier differs).
     int32_t G, rank, virt;
     int32_t nb;                 // CTAs per rank
+    int32_t kl;                 // rows per rank buffer (debug bound checks)
     struct Rank {
         int32_t *ped[2];        // [Kl]      PED of the nodes of a level
         uint32_t *used[2];      // [Kl][W]   rows of the nodes of level L live in buffer L & 1
@@ -217,6 +218,13 @@ __device__ int large_child_scalar(const LargeArgs &a, int d, const int32_t *pq, 
 template <typename T>
 __device__ __forceinline__ T *fg_loc(T *p, int64_t off) { return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + off); }
 
+#ifdef FG_DEBUG_CHECKS
+// debug builds only: a violated bound is reported once and counted (tests then see wrong results)
+__device__ unsigned int fg_dbg_bad;
+#define FG_CHECK(cond, ...) do { if (!(cond)) { if (atomicAdd(&fg_dbg_bad, 1u) == 0) printf(__VA_ARGS__); } } while (0)
+#else
+#define FG_CHECK(cond, ...) do { } while (0)
+#endif
 #ifdef FG_LSTAT
 __device__ unsigned long long fg_lstat[2];
 #endif
@@ -433,6 +441,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 auto issue = [&](int k, int dv, uint32_t *pf) {
                     const int64_t pl = __shfl_sync(FULL, dv, 0); // the parent's row on its rank
                     const int po = drank(__shfl_sync(FULL, dv, 1));
+                    FG_CHECK(k >= cb1 || (po >= 0 && po < G && pl >= 0 && pl < a.kl), "DBG parent i=%d k=%d po=%d pl=%lld\n", i, k, po,
+                             (long long)pl);
                     if (lane < 3) pf[PFW - 4 + 1 + lane] = (uint32_t)dv;
                     if (lane == 0) pf[PFW - 4] = (uint32_t)k;
                     if (k < cb1) {
@@ -595,6 +605,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     #pragma unroll
                             for (int b = 0; b < 4; ++b)
                                 if ((bal[b] >> lane) & 1u) {
+                                    FG_CHECK(pos >= 0 && pos < cs, "DBG list i=%d k=%d pos=%d\n", i, k, pos);
                                     crow[pos] = (uint8_t)(word >> (8 * b));
                                     trow[pos++] = (uint16_t)(u0 + b);
                                 }
@@ -774,6 +785,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 // its descriptor goes to its owner (a peer when sharded); the parent is row k of this rank
                 const int no = rowner(pos, Nn);
                 const int np = pos - rstart(Nn, no);
+                FG_CHECK(no >= 0 && no < G && np >= 0 && np < a.kl && pos < Nn, "DBG emit i=%d pos=%d Nn=%d no=%d np=%d\n", i, pos, Nn, no, np);
                 RK(no, sel_p)[np] = k;
                 RK(no, sel_j)[np] = u | (RANK << 16);
                 RK(no, sel_ped)[np] = ped;
@@ -925,6 +937,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         }
         if (!xsync()) return;
         if (home0() && threadIdx.x == 31) a.out[9] = nhist;
+#ifdef FG_DEBUG_CHECKS
+        if (home0() && threadIdx.x == 0 && fg_dbg_bad) printf("DBG violations %u\n", fg_dbg_bad);
+#endif
 #ifdef FG_LSTAT
         if (home0() && threadIdx.x == 0)
             printf("LSTAT parents with a survivor %llu of %llu (%.3f)\n", fg_lstat[0], fg_lstat[1], (double)fg_lstat[0] / fg_lstat[1]);
