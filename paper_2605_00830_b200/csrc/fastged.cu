@@ -139,6 +139,7 @@ struct fastged_batch {
     int n1max = 0, n2max = 0;
     DevBuf blob, ddesc, dorder, dcost, dmap, dchild, dpar, dalg, dwork;
     HostPinned stage; // this batch's pinned staging (inputs, order, results): batches can be in flight together
+    cudaEvent_t ev_h2d = nullptr; // the inputs' H2D copies (on the handle's copy stream) are complete
     size_t ord_at = 0, res_at = 0; // byte offsets of the order and result areas in `stage`
     int32_t pair_base = 0;         // index of pair 0 in the caller's arrays (error messages)
     std::map<GroupKey, std::vector<int32_t>> groups; // pair indices per kernel variant
@@ -179,6 +180,7 @@ struct fastged_handle {
     // batched launches of the word-width groups run concurrently (fork/join on side streams), so the
     // tail of one group's persistent launch overlaps the next group's start
     std::vector<cudaStream_t> gstreams;
+    cudaStream_t cstream = nullptr; // batch inputs' H2D copies: a chunk's upload overlaps the previous chunk's search
     std::vector<cudaEvent_t> gevents; // [0] fork, [1..] joins
 };
 
@@ -410,6 +412,7 @@ void free_batch(fastged_batch *b) {
     b->blob.release(); b->ddesc.release(); b->dorder.release(); b->dcost.release();
     b->dchild.release(); b->dpar.release(); b->dalg.release(); b->dmap.release(); b->dwork.release();
     b->stage.release();
+    if (b->ev_h2d) cudaEventDestroy(b->ev_h2d);
     delete b;
 }
 
@@ -494,14 +497,20 @@ fastged_batch *build_batch(fastged_handle_t *h, int32_t npairs, const fastged_gr
         CK(b->dalg.reserve(8 * (size_t)std::max(npairs, 1)));
         CK(b->dmap.reserve(4 * (size_t)std::max<int64_t>(b->total_map, 1)));
         CK(b->dwork.reserve(64 * sizeof(int)));
-        if (blob_bytes) CK(cudaMemcpyAsync(b->blob.p, stage, blob_bytes, cudaMemcpyHostToDevice, h->stream));
+        // the copies go on the copy stream (run_batch orders the batch's kernels after them), so a pipelined
+        // chunk's upload overlaps the search of the chunk before it
+        if (!h->cstream) CK(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+        if (!b->ev_h2d) CK(cudaEventCreateWithFlags(&b->ev_h2d, cudaEventDisableTiming));
+        if (blob_bytes) CK(cudaMemcpyAsync(b->blob.p, stage, blob_bytes, cudaMemcpyHostToDevice, h->cstream));
         if (npairs) CK(cudaMemcpyAsync(b->ddesc.p, stage + blob_bytes, sizeof(fg::PairDesc) * npairs,
-                                       cudaMemcpyHostToDevice, h->stream));
+                                       cudaMemcpyHostToDevice, h->cstream));
+        CK(cudaEventRecord(b->ev_h2d, h->cstream));
         h->stats.h2d_bytes += (int64_t)(blob_bytes + sizeof(fg::PairDesc) * npairs);
         return b; // b->stage stays in use until the stream passes the copies (the next sync on it)
     } catch (...) {
         if (!reuse) {
             cudaStreamSynchronize(h->stream);
+            if (h->cstream) cudaStreamSynchronize(h->cstream);
             free_batch(b);
         }
         throw;
@@ -753,6 +762,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         h->stats.branch_ms = 0.f;
     }
     if (first) CK(cudaEventRecord(h->ev_begin, h->stream));
+    if (b->ev_h2d) CK(cudaStreamWaitEvent(h->stream, b->ev_h2d, 0)); // the batch's inputs are on the device
     if (upload_order && !b->order_all.empty()) {
         // the order goes behind the blob in this batch's staging (the blob's bytes may still be in flight)
         uint8_t *ord = (uint8_t *)b->stage.p + b->ord_at;
@@ -1247,6 +1257,7 @@ void fastged_destroy(fastged_handle_t *h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->cstream) cudaStreamSynchronize(h->cstream);
     for (void *p : h->peer_base)
         if (p) cudaIpcCloseMemHandle(p);
     h->peer_base.clear();
@@ -1265,6 +1276,10 @@ void fastged_destroy(fastged_handle_t *h) {
     if (h->ev_end) cudaEventDestroy(h->ev_end);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     for (cudaStream_t gs : h->gstreams) cudaStreamDestroy(gs);
+    if (h->cstream) {
+        cudaStreamSynchronize(h->cstream);
+        cudaStreamDestroy(h->cstream);
+    }
     for (cudaEvent_t e : h->gevents) cudaEventDestroy(e);
     delete h;
 }
@@ -1326,6 +1341,7 @@ void fastged_batch_free(fastged_handle_t *h, fastged_batch_t *b) {
     if (h) {
         cudaSetDevice(h->device);
         if (h->stream) cudaStreamSynchronize(h->stream);
+        if (h->cstream) cudaStreamSynchronize(h->cstream);
     }
     free_batch(b);
 }
