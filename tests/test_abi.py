@@ -65,3 +65,16 @@ def test_built_for_sm100a(lib):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", binding.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_flag_constants_match_header():
+    """The binding's flag values are the header's (FASTGED_FLAG_*; the approximate top-K shift in bits 8..11)."""
+    from paper_2605_00830_b200 import binding
+    src = open(os.path.join(ROOT, "include", "fastged.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define FASTGED_FLAG_([A-Z_]+) (\d+)u", src)}
+    for name in ("TIMING", "DEBUG_WINDOW", "FORCE_LARGE", "VIRTUAL_SHARDS", "LAST_BY_TOTAL"):
+        assert getattr(binding, "FLAG_" + name) == vals[name], name
+    assert re.search(r"#define FASTGED_FLAG_APPROX\(shift\) \(\(uint32_t\)\(\(shift\) & 15\) << 8\)", src)
+    assert [binding.FLAG_APPROX(s) for s in (0, 1, 15)] == [0, 256, 15 << 8]
+    from oracle import oracle
+    assert [oracle.APPROX(s) for s in (0, 1, 15)] == [0, 256, 15 << 8]
