@@ -575,17 +575,23 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             uint32_t word = 0;
     #pragma unroll
                             for (int b = 0; b < 4; ++b) {
-                                const int u = u0 + b;
-                                // branch-free: every slot's value is computed, then the deletion slot and the
-                                // used / out-of-range slots are selected in
+                                // every slot's value is computed branch-free; the deletion slot and the used /
+                                // out-of-range slots are set below, once per word
                                 const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
                                               (LAB ? c.esub * ms[b] : 0);
                                 // rank code: x = PED - base + 1; approximate variant: PED bins of 2^ashift
-                                int cd = APX ? (x <= 0 ? 0 : min(((x - 1) >> a.ashift) + 1, win + 1)) : min(max(x, 0), win + 1);
-                                cd = (u == n2) ? cdel : cd; // deletion child (reading C5)
-                                cd = (u > n2 || (u < n2 && ((ub >> b) & 1u))) ? CODE_INVALID : cd;
+                                const int cd = APX ? (x <= 0 ? 0 : min(((x - 1) >> a.ashift) + 1, win + 1)) : min(max(x, 0), win + 1);
                                 word |= (uint32_t)cd << (8 * b);
                             }
+                            // slot n2 - u0 (if 0..3) is the deletion child (reading C5); slots of used
+                            // targets and past n2 are CODE_INVALID (bytes 0xff)
+                            const int rel = n2 - u0;
+                            uint32_t inv4 = ub;
+                            if (rel < 4) {
+                                inv4 = (ub & (rel <= 0 ? 0u : (1u << rel) - 1u)) | (rel < 0 ? 0xfu : ((0xeu << rel) & 0xfu));
+                                if (rel >= 0) word = (word & ~(0xffu << (8 * rel))) | ((uint32_t)cdel << (8 * rel));
+                            }
+                            word |= ((inv4 * 0x00204081u) & 0x01010101u) * 0xffu;
                             // histogram of the codes that can be selected (1..capc), per lane column
                             uint32_t hmk = bytes_lt(word, capc1) & ~bytes_eq(word, 0u);
                             while (hmk) {
