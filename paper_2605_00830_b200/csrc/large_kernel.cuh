@@ -603,19 +603,21 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             const uint32_t validb = ~bytes_eq(word, 0xffffffffu) & 0x80808080u;
                             const uint32_t listedb = listall ? validb : bytes_lt(word, capc1); // (255 > capc: never listed)
                             dropped |= (validb & ~listedb) != 0u;
-                            unsigned bal[4];
-    #pragma unroll
-                            for (int b = 0; b < 4; ++b) bal[b] = __ballot_sync(FULL, (listedb >> (8 * b + 7)) & 1u);
-                            // list entries in target order (u = 128 s + 4 lane + b: lanes first, then b)
-                            int pos = nsel + __popc(bal[0] & lml) + __popc(bal[1] & lml) + __popc(bal[2] & lml) + __popc(bal[3] & lml);
-    #pragma unroll
-                            for (int b = 0; b < 4; ++b)
-                                if ((bal[b] >> lane) & 1u) {
-                                    FG_CHECK(pos >= 0 && pos < cs, "DBG list i=%d k=%d pos=%d\n", i, k, pos);
-                                    crow[pos] = (uint8_t)(word >> (8 * b));
-                                    trow[pos++] = (uint16_t)(u0 + b);
-                                }
-                            nsel += __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
+                            // list entries in target order (u = 128 s + 4 lane + b: lanes first, then b): the
+                            // lane's listed count (0..4) as three ballot bit planes gives its offset in the warp
+                            uint32_t m4 = ((((listedb >> 7) & 0x01010101u) * 0x01020408u) >> 24) & 0xfu; // bit b: byte b listed
+                            const int cnt = __popc(m4);
+                            const unsigned B0 = __ballot_sync(FULL, cnt & 1), B1 = __ballot_sync(FULL, cnt & 2),
+                                           B2 = __ballot_sync(FULL, cnt & 4);
+                            int pos = nsel + __popc(B0 & lml) + 2 * __popc(B1 & lml) + 4 * __popc(B2 & lml);
+                            while (m4) {
+                                const int b = __ffs(m4) - 1;
+                                m4 &= m4 - 1;
+                                FG_CHECK(pos >= 0 && pos < cs, "DBG list i=%d k=%d pos=%d\n", i, k, pos);
+                                crow[pos] = (uint8_t)(word >> (8 * b));
+                                trow[pos++] = (uint16_t)(u0 + b);
+                            }
+                            nsel += __popc(B0) + 2 * __popc(B1) + 4 * __popc(B2);
                         }
                     };
                     if (a.ashift) slots(std::true_type{});
