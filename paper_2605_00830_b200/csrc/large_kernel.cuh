@@ -558,7 +558,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                                 int4 *dp = reinterpret_cast<int4 *>(D + u0);
                                 const int4 dv = *dp;
                                 *dp = make_int4(0, 0, 0, 0);
-                                cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff;
+                                if (LAB) { cb[0] = dv.x & 0xffff; cb[1] = dv.y & 0xffff; cb[2] = dv.z & 0xffff; cb[3] = dv.w & 0xffff; }
+                                else { cb[0] = dv.x; cb[1] = dv.y; cb[2] = dv.z; cb[3] = dv.w; } // (no mismatch half)
                                 if (LAB) { ms[0] = dv.x >> 16; ms[1] = dv.y >> 16; ms[2] = dv.z >> 16; ms[3] = dv.w >> 16; }
                             } else {
                                 uint32_t m = nzb;
