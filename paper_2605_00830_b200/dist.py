@@ -5,9 +5,11 @@ Two modes:
 * Batches of independent pairs: pair k goes to rank k mod world (``shard_pairs``); each rank runs
   ``fastged_solve_batch`` on its own GPU with no data-path collective; ``gather_results`` brings
   the per-rank results back to rank 0 in global pair order (``solve_batch_sharded`` = both).
-* One large pair: ``sharded_handle`` creates a handle whose frontier is split by parent across
-  all ranks; rank 0 creates the 128-byte ncclUniqueId (``binding.nccl_unique_id``) and
-  torch.distributed broadcasts it; every rank then calls ``solve_pair`` collectively.
+* One large pair: ``sharded_handle`` creates a handle whose frontier is split into equal slices over
+  all ranks (one GPU each, peer access over NVLink); rank 0 creates the 128-byte ncclUniqueId
+  (``binding.nccl_unique_id``) and torch.distributed broadcasts it; every rank then calls ``solve_pair``
+  collectively.  NCCL only bootstraps (CUDA IPC handles, two stream barriers per call): the per-level
+  exchange runs inside the sharded kernel over peer memory.
 """
 from __future__ import annotations
 
