@@ -283,14 +283,15 @@ bool fits_batched(int n1, int n2, int64_t k, int nlab) {
     return Kc * csmax < lim && (int64_t)batched_work_bytes(Kc, W, csmax) < lim && Kc * n1s < lim;
 }
 
-// Size routing by work: a batch with fewer pairs than SMs leaves most of the GPU idle under the batched
-// kernel (one CTA per pair), so a pair whose levels are wide -- frontier cap x (n2 + 1) candidates above
-// WHOLE_GPU_CANDIDATES -- runs on the whole-GPU kernel instead (measured, scripts/paper_points.py: one
-// 20-vertex pair at K = 7e5 takes 399 ms on one CTA and 12.5 ms on the whole GPU; at K = 1000 the one
-// CTA wins, 0.35 vs 0.61 ms, the grid barriers of ~20 levels costing more than the work).
-constexpr int64_t WHOLE_GPU_CANDIDATES = 1 << 16;
-bool prefers_whole_gpu(int n1, int n2, int64_t k, int64_t npairs, int sms) {
-    return npairs < sms && frontier_cap(n1, n2, k) * (int64_t)(n2 + 1) > WHOLE_GPU_CANDIDATES;
+// Work routing: the batched kernel gives a pair one CTA, the whole-GPU kernel the whole GPU for one pair at a
+// time.  A pair with wide levels (frontier cap x (n2 + 1) candidates) gains up to ~32x from the whole GPU
+// (scripts/paper_points.py: one 20-vertex pair at K = 7e5 takes 399 ms on one CTA and 12.6 ms on the whole
+// GPU; n = 50 at K = 5000: 9.1 vs 1.9 ms), but a batch of such pairs keeps every SM busy on the batched
+// kernel.  Estimated gain g = min(32, candidates / 2^16); the whole GPU is chosen while npairs <= g / 2 (a
+// single pair: above 131,072 candidates per level; at K = 1000 and n = 20 the one CTA wins, 0.35 vs 0.61 ms).
+bool prefers_whole_gpu(int n1, int n2, int64_t k, int64_t npairs) {
+    const int64_t cand = frontier_cap(n1, n2, k) * (int64_t)(n2 + 1);
+    return 2 * npairs * ((int64_t)1 << 16) <= std::min<int64_t>(32ll << 16, cand);
 }
 
 // Number of distinct g2 edge labels (the label planes of a labelled pair).
@@ -634,7 +635,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
         if (fits_batched(d.n1, d.n2, k, d.labelled ? d.nlab : 0) && !(h->flags & FASTGED_FLAG_FORCE_LARGE) &&
             !(h->flags & FASTGED_FLAG_APPROX_MASK) &&
-            !(prefers_whole_gpu(d.n1, d.n2, k, b->npairs, h->sms) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL)))
+            !(prefers_whole_gpu(d.n1, d.n2, k, b->npairs) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL)))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
             b->large.push_back(p); // solved by the whole-GPU kernel after the batched launches
@@ -1443,7 +1444,7 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
         }
         if (!fits_batched(g1->n, g2->n, k, labelled_pair(g1, g2) ? g2_label_count(g2) : 0) ||
             (h->flags & (FASTGED_FLAG_FORCE_LARGE | FASTGED_FLAG_APPROX_MASK)) ||
-            (prefers_whole_gpu(g1->n, g2->n, k, 1, h->sms) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL))) {
+            (prefers_whole_gpu(g1->n, g2->n, k, 1) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL))) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }
