@@ -983,7 +983,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const bool wide = n2 > 254;          // lambda entries: uint16 (255 would collide with "deleted")
     const bool c16 = maxdeg > 255;       // counters: uint16 when a degree does not fit a byte
     const int esz = wide ? 2 : 1, csz = c16 ? 2 : 1;
-    const int n1s = wide ? std::max(2, (n1 + 1) & ~1) : std::max(4, (n1 + 3) & ~3);
+    // lambda row stride: a 16-byte multiple (the kernel moves rows in 16-byte chunks)
+    const int n1s = wide ? std::max(8, (n1 + 7) & ~7) : std::max(16, (n1 + 15) & ~15);
     int dmax = 0;
     {
         std::vector<int> dd(n1 + 1, 0);

@@ -451,7 +451,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         for (int x = lane; x < CNTW / 4; x += 32) cpa16(pf + 4 * x, crow8 + 16 * x);
                         for (int w = lane; w < W; w += 32) cpa4(pf + CNTW + w, RK(po, used[pv]) + pl * W + w);
                         const uint32_t *mr = reinterpret_cast<const uint32_t *>(RK(po, map[pv])) + pl * rowwords;
-                        for (int w = lane; w < wprev; w += 32) cpa4(pf + CNTW + 32 + w, mr + w);
+                        // lambda row in 16-byte chunks (rows are 16-byte multiples; the words past wprev are
+                        // never read as entries)
+                        for (int w = 4 * lane; w < wprev; w += 128) cpa16(pf + CNTW + 32 + w, mr + w);
                     }
                     cpa_commit(); // (possibly empty group: keeps the ring's group count uniform)
                 };
@@ -459,14 +461,16 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 issue(kn, dn, pfb);
                 kn = grab();
                 dn = load_desc(kn);
+                static_assert(LPF == 2, "the prefetch ring alternates two slots");
+                uint32_t *pf = pfb, *pfn = pfb + PFW; // slot being expanded / slot being filled
                 for (int r = 0;; ++r) {
+                    if (r > 0) { uint32_t *t = pf; pf = pfn; pfn = t; } // (the slot expanded last is refilled)
                     const int kx = kn, dx = dn;
                     kn = grab();
                     dn = load_desc(kn);                               // descriptor of the parent after next
-                    issue(kx, dx, pfb + ((r + 1) % LPF) * PFW);       // rows of the next parent
+                    issue(kx, dx, pfn);                               // rows of the next parent
                     cpa_wait<1>();
                     __syncwarp();
-                    uint32_t *pf = pfb + (r % LPF) * PFW;
                     const int k = (int)pf[PFW - 4];
                     if (k >= cb1) break; // (parents are taken in increasing order: the rest is empty)
                     const int j = dtarget((int32_t)pf[PFW - 2]), pedp = (int)pf[PFW - 1];
@@ -489,13 +493,22 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         const int hw = (i - 1) / EPW, sh = ((i - 1) % EPW) * 8 * ESZ;
                         const uint32_t e = (j == n2) ? (uint32_t)DELV : (uint32_t)j;
                         uint32_t *dst = reinterpret_cast<uint32_t *>(Qmap) + (int64_t)k * rowwords;
-                        for (int w = lane; w < wcur; w += 32) {
-                            uint32_t word = w < wprev ? mrow[w] : 0u;
-                            if (w == hw) {
+                        for (int w = 4 * lane; w < wcur; w += 128) { // 16-byte chunks
+                            uint4 v = w < wprev ? *reinterpret_cast<const uint4 *>(mrow + w) : make_uint4(0u, 0u, 0u, 0u);
+                            if ((unsigned)(hw - w) < 4u) {
+                                uint32_t *vw = reinterpret_cast<uint32_t *>(&v);
+                                uint32_t word = vw[0];
+                                if (hw - w == 1) word = vw[1];
+                                if (hw - w == 2) word = vw[2];
+                                if (hw - w == 3) word = vw[3];
                                 word = (word & ~((uint32_t)DELV << sh)) | (e << sh);
-                                mrow[w] = word;
+                                mrow[hw] = word;
+                                if (hw - w == 0) v.x = word;
+                                if (hw - w == 1) v.y = word;
+                                if (hw - w == 2) v.z = word;
+                                if (hw - w == 3) v.w = word;
                             }
-                            dst[w] = word;
+                            *reinterpret_cast<uint4 *>(dst + w) = v;
                         }
                     }
                     __syncwarp();

@@ -534,3 +534,18 @@ def test_sharded_virtual_large_pair(fg, handle):
     r = h.solve_pair(g1, g2, COSTS["setting1"], 2000, levels=True)
     h.close()
     assert r["cost"] == ref["cost"] and np.array_equal(r["mapping"], ref["mapping"]) and r["levels"] == ref["levels"]
+
+
+def test_work_routing_single_wide_pair(fg, oracle):
+    """A single pair with wide levels runs on the whole-GPU kernel (its phase clocks are set), a narrow one on
+    the batched kernel; both give the oracle's result (prefers_whole_gpu)."""
+    rng = synth.rng_for(808)
+    g1, g2 = synth.er_graph(rng, 20, 0.4, 4), synth.er_graph(rng, 20, 0.4, 4)
+    h = fg.Handle(0)
+    for K, whole in ((1000, False), (200_000, True)):
+        r = h.solve_pair(g1, g2, COSTS["setting1"], K)
+        st = h.stats()
+        assert (sum(st["phase_ms"]) > 0) == whole, (K, st["phase_ms"])
+        o = oracle.kbest(g1, g2, COSTS["setting1"], K)
+        assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]) and r["children"] == o["children"]
+    h.close()
