@@ -522,14 +522,15 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             const int kk = k0 + lane;
                             const int tk = kk < d ? tmap(s_pq[kk]) : DELV;
                             const int lk = (LAB && kk < d) ? s_pl[kk] : 0;
+                            // the neighbour-list range of this lane's image, loaded for all images at once
+                            // (a deleted image has an empty range)
+                            const int bk = tk != DELV ? nptr[tk] : 0, ek = tk != DELV ? nptr[tk + 1] : 0;
                             const int kn2 = min(32, d - k0);
                             for (int z = 0; z < kn2; ++z) {
-                                const int t = __shfl_sync(FULL, tk, z);
-                                if (t == DELV) continue;
+                                const int e0 = __shfl_sync(FULL, bk, z), e1 = __shfl_sync(FULL, ek, z);
                                 const int lz = LAB ? __shfl_sync(FULL, lk, z) : 0;
-                                const int e1 = nptr[t + 1];
                                 // the neighbours of one t are distinct: plain read-modify-write, no atomics
-                                for (int e = nptr[t] + lane; e < e1; e += 32) {
+                                for (int e = e0 + lane; e < e1; e += 32) {
                                     const uint32_t v = nbr[e];
                                     D[v & 0xffffu] += (LAB && (int)(v >> 16) != lz) ? 0x10001 : 1;
                                 }
