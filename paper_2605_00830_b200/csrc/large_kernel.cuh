@@ -965,7 +965,8 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
 #endif
 #ifdef FG_LSTAT
         if (home0() && threadIdx.x == 0)
-            printf("LSTAT parents with a survivor %llu of %llu (%.3f)\n", fg_lstat[0], fg_lstat[1], (double)fg_lstat[0] / fg_lstat[1]);
+            printf("LSTAT parents with a survivor %llu of %llu (%.3f); A passes %d over %d levels\n", fg_lstat[0], fg_lstat[1],
+                   (double)fg_lstat[0] / fg_lstat[1], ps, n1);
 #endif
         if (home0()) {
             const unsigned long long best = *a.best;
