@@ -1,3 +1,5 @@
+"""Whole-GPU kernel on dense and sparse large pairs (n = 500 / 950, density 0.05 / 0.4, K = 5000): device time
+and the phase split (A+T, B, C1) -- the cB popcount path dominates A on dense g2."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 from paper_2605_00830_b200 import binding, synth, build
