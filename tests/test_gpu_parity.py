@@ -549,3 +549,20 @@ def test_work_routing_single_wide_pair(fg, oracle):
         o = oracle.kbest(g1, g2, COSTS["setting1"], K)
         assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]) and r["children"] == o["children"]
     h.close()
+
+
+def test_whole_gpu_and_sharded_degenerate_pairs(fg, oracle):
+    """Empty and one-vertex graphs through the whole-GPU kernel and 3 virtual ranks of the sharded kernel (most
+    ranks then own empty slices of the one-node levels): the oracle's cost and mapping (readings C16, C5)."""
+    hl = fg.Handle(0, flags=fg.FLAG_FORCE_LARGE)
+    hs = fg.Handle(0, world_size=3, flags=fg.FLAG_VIRTUAL_SHARDS)
+    rng = synth.rng_for(909)
+    for n1, n2 in ((0, 0), (0, 5), (5, 0), (1, 1), (1, 7), (7, 1), (2, 2)):
+        g1, g2 = synth.er_graph(rng, n1, 0.5, 2), synth.er_graph(rng, n2, 0.5, 2)
+        for K in (1, 3, 100):
+            o = oracle.kbest(g1, g2, COSTS["setting1"], K)
+            for h in (hl, hs):
+                r = h.solve_pair(g1, g2, COSTS["setting1"], K)
+                assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]), (n1, n2, K)
+    hl.close()
+    hs.close()
