@@ -58,8 +58,8 @@ extern "C" {
 #define FASTGED_FLAG_LAST_BY_TOTAL 16u /* method variant: rank the last level by
                                          PED + insertion completion instead of PED (the alternative to reading
                                          C10 of Alg. 1); never a higher cost than the
-                                         paper-literal rule.  Batched path only (n2 <= 128): a pair that needs
-                                         the whole-GPU or sharded path fails with FASTGED_ERR_ARG. */
+                                         paper-literal rule.  Every path (batched, whole-GPU, sharded); not
+                                         combined with FASTGED_FLAG_APPROX (FASTGED_ERR_ARG). */
 /* method variant ("approximate top-k selection may become an option"
  * for extreme K): each level keeps the min(K, c_i) smallest children under the coarse key
  * (floor((PED - lo_i) / 2^shift), parent, child), lo_i = the smallest PED of the level's parents --

@@ -20,7 +20,7 @@ FLAG_TIMING = 1
 FLAG_DEBUG_WINDOW = 2
 FLAG_FORCE_LARGE = 4
 FLAG_VIRTUAL_SHARDS = 8
-FLAG_LAST_BY_TOTAL = 16  # method variant: last level ranked by PED + completion (batched path only)
+FLAG_LAST_BY_TOTAL = 16  # method variant: last level ranked by PED + completion (every path)
 
 
 def FLAG_APPROX(shift: int) -> int:

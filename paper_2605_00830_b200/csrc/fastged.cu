@@ -635,7 +635,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
             fail(FASTGED_ERR_OVERFLOW, "pair %d: worst-case PED %lld does not fit int32", b->pair_base + p, (long long)bound);
         if (fits_batched(d.n1, d.n2, k, d.labelled ? d.nlab : 0) && !(h->flags & FASTGED_FLAG_FORCE_LARGE) &&
             !(h->flags & FASTGED_FLAG_APPROX_MASK) &&
-            !(prefers_whole_gpu(d.n1, d.n2, k, b->npairs) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL)))
+            !prefers_whole_gpu(d.n1, d.n2, k, b->npairs))
             b->groups[GroupKey{b->W[p], d.labelled != 0}].push_back(p);
         else
             b->large.push_back(p); // solved by the whole-GPU kernel after the batched launches
@@ -933,8 +933,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     if (real && !h->comm) fail(FASTGED_ERR_NCCL, "the handle's NCCL communicator was aborted by an earlier failure");
     if (dst && G > 1) fail(FASTGED_ERR_ARG, "internal: a batch pair is never sharded");
     const int n1 = g1->n, n2 = g2->n;
-    if (h->flags & FASTGED_FLAG_LAST_BY_TOTAL)
-        fail(FASTGED_ERR_ARG, "FASTGED_FLAG_LAST_BY_TOTAL is implemented on the batched path only (n2 <= 128)");
+    if ((h->flags & FASTGED_FLAG_LAST_BY_TOTAL) && (h->flags & FASTGED_FLAG_APPROX_MASK))
+        fail(FASTGED_ERR_ARG, "FASTGED_FLAG_LAST_BY_TOTAL and FASTGED_FLAG_APPROX are exclusive");
     if (n2 > FASTGED_MAX_N2) fail(FASTGED_ERR_CAPACITY, "target graph has n2=%d > %d (limit of this build)", n2, FASTGED_MAX_N2);
     const int64_t Kc64 = frontier_cap(n1, n2, k);
     if (Kc64 > (int64_t)1 << 30) fail(FASTGED_ERR_CAPACITY, "frontier cap %lld too large", (long long)Kc64);
@@ -1102,6 +1102,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     a.K = Kc;
     a.win = (h->flags & FASTGED_FLAG_DEBUG_WINDOW) ? 2 : 253;
     a.ashift = (int32_t)((h->flags & FASTGED_FLAG_APPROX_MASK) >> 8);
+    a.last_by_total = (h->flags & FASTGED_FLAG_LAST_BY_TOTAL) ? 1 : 0;
     a.W = W;
     a.cs = cs;
     a.S = cs / 128;
@@ -1445,7 +1446,7 @@ int fastged_solve_pair_ex(fastged_handle_t *h, const fastged_graph_t *g1, const 
         }
         if (!fits_batched(g1->n, g2->n, k, labelled_pair(g1, g2) ? g2_label_count(g2) : 0) ||
             (h->flags & (FASTGED_FLAG_FORCE_LARGE | FASTGED_FLAG_APPROX_MASK)) ||
-            (prefers_whole_gpu(g1->n, g2->n, k, 1) && !(h->flags & FASTGED_FLAG_LAST_BY_TOTAL))) {
+            prefers_whole_gpu(g1->n, g2->n, k, 1)) {
             solve_large(h, g1, g2, c, k, out, levels_out);
             return FASTGED_OK;
         }

@@ -120,6 +120,7 @@ struct LargeArgs {
     Costs c;
     int32_t K, win, W;
     int32_t ashift;         // method variant (NEXT-4): approximate top-K with PED bins of 2^ashift (0 = exact)
+    int32_t last_by_total;  // method variant (NEXT-4, reading C10 alternative): the last level ranked by PED + completion
     int32_t cs, S;          // row stride of codes / counters (multiple of 128 >= n2 + 1); S = cs / 128
     int32_t n1s;            // lambda row stride in elements (4-byte multiple)
     int32_t n1r;            // staged P_i list capacity in shared memory (>= max d, multiple of 4)
@@ -412,13 +413,17 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         // the children whose code can be selected (<= capc); a level that keeps everything although
         // children were left out is redone with complete lists (rare: N == K and one child per parent)
         bool listall = N < K;
+        // method variant: the last level ranked by total = PED + insertion completion; a child's
+        // completion is its parent's minus vins and eins per used neighbour of its target, so the eins cnt
+        // term of its PED cancels: total = PED_p + comp_p - vins + cv + edel d - (edel + eins) cB (+ mis)
+        const bool lastTot = a.last_by_total && i == n1 - 1;
         int tcode = 0, rq = 0;
         block_sync(); // P_i staged
 
         for (;;) { // ---------------- A + T ----------------
             // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
             // (each of the N parents has a deletion child <= U_i): their codes skip the histogram.
-            const int capc = (N >= K) ? max(0, min(win, ((hi + pedDel - base) >> a.ashift) + 1)) : win;
+            const int capc = (N >= K && !lastTot) ? max(0, min(win, ((hi + pedDel - base) >> a.ashift) + 1)) : win;
             const uint32_t capc1 = (uint32_t)(capc + 1) * 0x01010101u; // (capc + 1 <= win + 1 <= 254)
             for (int k = threadIdx.x; k < 256 * 32; k += LNT) s_hist[k] = 0;
             if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; s_drop = 0; }
@@ -546,9 +551,25 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         nzb = __ballot_sync(FULL, lane < W && sB[lane] != 0u);
                     }
                     __syncwarp();
-                    const int pb = pedp - base + 1 + edd;
-                    const int xdel = pedp + pedDel - base + 1;
-                    const int cdel = a.ashift ? (xdel <= 0 ? 0 : min(((xdel - 1) >> a.ashift) + 1, win + 1)) : rank_code(pedp + pedDel, base, win);
+                    int comp = 0; // (variant, last level) this node's insertion completion
+                    if (lastTot) {
+                        int e2u2 = 0; // used-neighbour counters summed over the used targets: 2 x edges among them
+                        for (int s = 0; s < S; ++s) {
+                            const int u0 = 128 * s + 4 * lane, wu = u0 >> 5;
+                            typename C4::V cv = C4::load(reinterpret_cast<const CntT *>(pf), u0);
+                            if (jn >= 0 && wu < W) cv = C4::add_bits(cv, (adjw(jn, wu) >> (u0 & 31)) & 0xfu);
+                            const uint32_t ub = wu < W ? (sU[wu] >> (u0 & 31)) & 0xfu : 0u;
+#pragma unroll
+                            for (int b = 0; b < 4; ++b)
+                                if ((ub >> b) & 1u) e2u2 += C4::get(cv, b);
+                        }
+                        e2u2 = __reduce_add_sync(FULL, e2u2);
+                        comp = c.vins * (n2 - nused) + c.eins * (pd.m2 - e2u2 / 2);
+                    }
+                    const int pb = pedp - base + 1 + edd + (lastTot ? comp - c.vins : 0);
+                    const int einsT = lastTot ? 0 : c.eins;
+                    const int xdel = pedp + pedDel + comp - base + 1;
+                    const int cdel = a.ashift ? (xdel <= 0 ? 0 : min(((xdel - 1) >> a.ashift) + 1, win + 1)) : rank_code(pedp + pedDel + comp, base, win);
                     uint8_t *crow = ML(ccode) + (int64_t)k * cs;
                     uint16_t *trow = ML(ctgt) + (int64_t)k * cs;
                     const CntT *cr = reinterpret_cast<const CntT *>(pf);
@@ -592,7 +613,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                             for (int b = 0; b < 4; ++b) {
                                 // every slot's value is computed branch-free; the deletion slot and the used /
                                 // out-of-range slots are set below, once per word
-                                const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + c.eins * C4::get(cv, b) - ee * cb[b] +
+                                const int x = pb + (int)((mnib >> b) & 1u) * c.vsub + einsT * C4::get(cv, b) - ee * cb[b] +
                                               (LAB ? c.esub * ms[b] : 0);
                                 // rank code: x = PED - base + 1; approximate variant: PED bins of 2^ashift
                                 const int cd = APX ? (x <= 0 ? 0 : min(((x - 1) >> a.ashift) + 1, win + 1)) : min(max(x, 0), win + 1);
@@ -802,9 +823,26 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             auto emit = [&](int k, int u, int code, int pos) {
                 int ped;
                 if (a.ashift == 0 && code >= 1 && code <= win) ped = base + code - 1;
-                else // below the window, saturated or a PED bin: recompute from the parent's materialised row
+                else { // below the window, saturated or a PED bin: recompute from the parent's materialised row
                     ped = large_child_scalar<MapT, CntT, LAB>(a, d, s_pq, s_pl, ML(ped[cu])[k], Qcnt + (int64_t)k * cs,
                                                               Qmap + (int64_t)k * a.n1s, u, adj2, e2, vl1i, vl2);
+                    if (lastTot) { // (variant) + the child's completion, from the node's used row and counters
+                        const uint32_t *ur = Qused + (int64_t)k * W;
+                        const CntT *cr2 = Qcnt + (int64_t)k * cs;
+                        int usedc = (u < n2) ? 1 : 0, e2u2 = 0;
+                        for (int w = 0; w < W; ++w) {
+                            uint32_t bits = ur[w];
+                            usedc += __popc(bits);
+                            while (bits) {
+                                const int t = 32 * w + __ffs(bits) - 1;
+                                bits &= bits - 1;
+                                e2u2 += (int)cr2[t];
+                            }
+                        }
+                        if (u < n2) e2u2 += 2 * (int)cr2[u];
+                        ped += c.vins * (n2 - usedc) + c.eins * (pd.m2 - e2u2 / 2);
+                    }
+                }
                 // its descriptor goes to its owner (a peer when sharded); the parent is row k of this rank
                 const int no = rowner(pos, Nn);
                 const int np = pos - rstart(Nn, no);
@@ -954,7 +992,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             usedc = __reduce_add_sync(FULL, usedc);
             e2u2 = __reduce_add_sync(FULL, e2u2); // every edge among used vertices counted from both ends
             if (lane == 0) {
-                const int64_t total = (int64_t)ped + (int64_t)c.vins * (n2 - usedc) + (int64_t)c.eins * (pd.m2 - e2u2 / 2);
+                // (variant: the last level already ranked and stored PED + completion; n1 = 0 has no last level)
+                const int64_t total = (a.last_by_total && n1 > 0)
+                                          ? (int64_t)ped
+                                          : (int64_t)ped + (int64_t)c.vins * (n2 - usedc) + (int64_t)c.eins * (pd.m2 - e2u2 / 2);
                 atomicMin(a.best, ((unsigned long long)total << 32) | (unsigned)(s0 + k));
             }
         }

@@ -3,7 +3,8 @@
 random ER / labelled pairs (n1, n2 in 1..48, densities 0.05..0.6, 1..4 vertex labels, 1..3 edge labels),
 random integer costs (0..9 each), random K (1..3000), through the batched kernel (one batch), the whole-GPU
 kernel (FASTGED_FLAG_FORCE_LARGE, with and without the 2-wide debug window), 3 virtual ranks of the sharded
-kernel, and the approximate top-K variant (s = 2, against the oracle's variant).
+kernel, the approximate top-K variant (s = 2) and the last-level-by-total variant on the whole-GPU kernel (each
+against the oracle's variant).
 
     python scripts/stress_parity.py [npairs] [out.json]
 """
@@ -35,14 +36,15 @@ def main(npairs, out):
     handles = {"whole_gpu": binding.Handle(0, flags=binding.FLAG_FORCE_LARGE),
                "whole_gpu_window2": binding.Handle(0, flags=binding.FLAG_FORCE_LARGE | binding.FLAG_DEBUG_WINDOW),
                "sharded_3_virtual": binding.Handle(0, world_size=3, flags=binding.FLAG_VIRTUAL_SHARDS),
-               "approx_s2": binding.Handle(0, flags=binding.FLAG_APPROX(2))}
+               "approx_s2": binding.Handle(0, flags=binding.FLAG_APPROX(2)),
+               "last_by_total_whole_gpu": binding.Handle(0, flags=binding.FLAG_FORCE_LARGE | binding.FLAG_LAST_BY_TOTAL)}
     bad = {k: [] for k in handles}
     bad["batched"] = []
     for k, ((g1, g2), K, c) in enumerate(zip(pairs, Ks, costs)):
         o = oracle.kbest(g1, g2, c, K)
         for name, h in handles.items():
-            if name == "approx_s2":
-                oa = oracle.kbest(g1, g2, c, K, flags=oracle.APPROX(2))
+            if name in ("approx_s2", "last_by_total_whole_gpu"):
+                oa = oracle.kbest(g1, g2, c, K, flags=oracle.APPROX(2) if name == "approx_s2" else oracle.LAST_BY_TOTAL)
                 r = h.solve_pair(g1, g2, c, K)
                 ok = r["cost"] == oa["cost"] and np.array_equal(r["mapping"], oa["mapping"]) and r["children"] == oa["children"]
             else:

@@ -248,8 +248,8 @@ def test_variant_approx_topk_matches_oracle(fg, oracle, shift, window):
 @pytest.mark.parametrize("window", [0, 2], ids=["window127", "window2"])
 def test_variant_last_by_total_matches_oracle(fg, oracle, window):
     """FASTGED_FLAG_LAST_BY_TOTAL (last level ranked by PED + completion, the alternative to reading C10)
-    against the oracle's variant, bit-exact, on ER, labelled molecule and n1 != n2 pairs; the whole-GPU
-    path refuses the flag."""
+    against the oracle's variant, bit-exact, on ER, labelled molecule and n1 != n2 pairs, through the batched,
+    whole-GPU and sharded kernels; combined with the approximate top-K flag it is refused."""
     flags = fg.FLAG_LAST_BY_TOTAL | (fg.FLAG_DEBUG_WINDOW if window else 0)
     h = fg.Handle(0, flags=flags)
     w3 = synth.config_workload(3, npairs=50, K=300)
@@ -266,11 +266,26 @@ def test_variant_last_by_total_matches_oracle(fg, oracle, window):
         for k in range(len(pairs)):
             assert gc[k] == oc[k] and np.array_equal(gm[k], om[k]) and gch[k] == och[k], k
             assert gc[k] <= lc[k]
-    g1, g2 = synth.large_pair(150, 0.1, seed=3)
+    # the whole-GPU kernel (n2 > 128, or forced) and 2 virtual ranks of the sharded kernel rank the last level the same way
+    hs = fg.Handle(0, world_size=2, flags=flags | fg.FLAG_VIRTUAL_SHARDS)
+    hf = fg.Handle(0, flags=flags | fg.FLAG_FORCE_LARGE)
+    rng2 = synth.rng_for(62, window)
+    cases = [synth.large_pair(150, 0.1, seed=3), synth.large_pair(140, 0.05, seed=4)] + \
+            [(synth.er_graph(rng2, int(rng2.integers(1, 40)), 0.3, 3, 1 + x % 2),
+              synth.er_graph(rng2, int(rng2.integers(1, 60)), 0.3, 3, 1 + x % 2)) for x in range(10)]
+    for x, (g1, g2) in enumerate(cases):
+        K = 100 if x < 2 else int(rng2.integers(1, 500))
+        o = oracle.kbest(g1, g2, COSTS["setting1"], K, levels=True, flags=oracle.LAST_BY_TOTAL)
+        for hh in (h, hs, hf):
+            r = hh.solve_pair(g1, g2, COSTS["setting1"], K, levels=True)
+            assert r["cost"] == o["cost"] and np.array_equal(r["mapping"], o["mapping"]), (x, K)
+            assert r["children"] == o["children"] and r["levels"] == [tuple(v) for v in o["levels"]], (x, K)
     with pytest.raises(fg.FastGedError) as e:
-        h.solve_pair(g1, g2, COSTS["setting1"], 100)
+        fg.Handle(0, flags=flags | fg.FLAG_APPROX(2)).solve_pair(*cases[0], COSTS["setting1"], 100)
     assert e.value.code == fg.ERR_ARG
     h.close()
+    hs.close()
+    hf.close()
 
 
 # ------------------------------------------------------------------ KNN_GED (NEXT-3)
