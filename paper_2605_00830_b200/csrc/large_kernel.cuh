@@ -53,6 +53,9 @@ namespace cg = cooperative_groups;
 #define FG_LNT 640
 #endif
 constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per SM)
+#ifndef FG_C1_LIGHT
+#define FG_C1_LIGHT 8 // C1: rows with at most this many survivors are emitted lane per row
+#endif
 #ifndef FG_LPF
 #define FG_LPF 2
 #endif
@@ -883,7 +886,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 const int rn = has ? ML(rown)[kl] : 0;
                 // rows with few survivors: lane per row (32 rows in flight); the rest: warp per row below
                 const int nkeep = keepall ? (rc & 0xffff) : (rc & 0xffff) + min(rc >> 16, max(0, rq - ep));
-                const bool light = has && nkeep <= 8;
+                const bool light = has && nkeep <= FG_C1_LIGHT;
                 hm &= ~__ballot_sync(FULL, light);
                 if (light) {
                     int out = lp + (keepall ? 0 : min(rq, ep)), eq_seen = ep, left = nkeep;
