@@ -45,6 +45,9 @@ namespace fg {
 #ifndef FG_MINBLOCKS
 #define FG_MINBLOCKS 2 // resident CTAs per SM requested from ptxas (A/B experiments)
 #endif
+#ifndef FG_MINBLOCKS_128
+#define FG_MINBLOCKS_128 4 // the same for the 128-thread (one-word) variants
+#endif
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAP_DEL = 255;      // lambda entry of a deleted g1 vertex
@@ -205,7 +208,7 @@ __device__ __forceinline__ int completion_of(const uint32_t (&U)[W], const uint3
 }
 
 template <int W, bool LAB, int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, FG_MINBLOCKS * 256 / NT) kbest_batch_kernel(const BatchArgs a) {
+__global__ void __launch_bounds__(NT, NT == 128 ? FG_MINBLOCKS_128 : FG_MINBLOCKS * 256 / NT) kbest_batch_kernel(const BatchArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     // per-warp rank-code histograms, row stride 132: code c at [c + 3], codes 1..128 16-byte aligned
     __shared__ __align__(16) int s_hist[(NT / 32) * 132];
