@@ -57,33 +57,47 @@ def gather_results(npairs: int, idx: np.ndarray, costs: np.ndarray, maps: np.nda
                    n1_all: Sequence[int], group=None) -> Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]]:
     """Collect (cost, mapping) of every pair on rank 0 in global pair order (None on other ranks).
 
-    idx: the global pair indices this rank solved; costs/maps/offs: its solve_batch outputs (flat
-    mappings, offsets per local pair).  Returns (costs int64[npairs], mappings int32 flat in global
-    pair order, offsets int64[npairs + 1]).  Mappings travel as int16 (g2 indices < 2^15).
+    idx: the global pair indices this rank solved (``shard_pairs``); costs/maps/offs: its solve_batch outputs
+    (flat mappings, offsets per local pair); n1_all: n1 of every global pair.  Every rank knows every rank's
+    pairs (pair r -> rank r mod world) and their mapping lengths, so one fixed-size tensor gather suffices:
+    each rank sends [costs as (lo, hi) int32 words | mappings int32] padded to the largest rank's length (on
+    the process group's device: NCCL ranks gather on their GPU).  Returns (costs int64[npairs], mappings int32
+    flat in global pair order, offsets int64[npairs + 1]).
     """
+    import torch
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    mp = np.asarray(maps)
-    wire = mp.astype(np.int16) if (mp.size == 0 or int(mp.max(initial=-1)) < 2 ** 15) else mp.astype(np.int32)
-    mine = (np.asarray(idx, np.int64), np.asarray(costs, np.int64), wire, np.asarray(offs, np.int64))
-    parts = [None] * world if rank == 0 else None
-    dist.gather_object(mine, parts, dst=0, group=group)
+    n1 = np.asarray(n1_all, np.int64)
+    parts = [shard_pairs(npairs, r, world) for r in range(world)]
+    if not np.array_equal(np.asarray(idx, np.int64), parts[rank]):
+        raise ValueError("gather_results: this rank's pairs are not shard_pairs(npairs, rank, world)")
+    lens = [2 * p.shape[0] + int(n1[p].sum()) for p in parts]
+    L = max(lens) if lens else 0
+    c = np.asarray(costs, np.int64)
+    mp = np.asarray(maps, np.int32)[: int(np.asarray(offs)[-1])] if len(offs) else np.zeros(0, np.int32)
+    if mp.shape[0] != int(n1[parts[rank]].sum()):
+        raise ValueError("gather_results: mapping length does not match the pairs' n1")
+    buf = np.zeros(max(L, 1), np.int32)
+    buf[: 2 * c.shape[0]] = c.view(np.int32)  # (little endian: lo, hi per cost)
+    buf[2 * c.shape[0]: 2 * c.shape[0] + mp.shape[0]] = mp
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(buf).to(dev)
+    recv = [torch.empty_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, recv, dst=0, group=group)
     if rank != 0:
         return None
-    n1 = np.asarray(n1_all, np.int64)
     goffs = np.zeros(npairs + 1, np.int64)
     goffs[1:] = np.cumsum(n1)
-    out_c = np.full(npairs, -1, np.int64)
-    out_m = np.full(int(goffs[-1]), -2, np.int32)
-    for pidx, pc, pm, po in parts:
-        out_c[pidx] = pc
-        lens = np.diff(po)
-        assert np.array_equal(lens, n1[pidx]), "a rank returned a mapping of the wrong length"
-        # destination of local entry t of local pair x: goffs[pidx[x]] + t
-        starts = np.repeat(goffs[pidx] - po[:-1], lens)
-        out_m[starts + np.arange(int(po[-1]))] = pm[: int(po[-1])]
-    assert (out_c >= 0).all(), "a pair was not solved by any rank"
-    assert not (out_m == -2).any(), "a mapping entry was not filled"
+    out_c = np.empty(npairs, np.int64)
+    out_m = np.empty(int(goffs[-1]), np.int32)
+    for r, (p, tr) in enumerate(zip(parts, recv)):
+        a = tr.cpu().numpy()
+        k = p.shape[0]
+        out_c[p] = a[: 2 * k].view(np.int64)
+        lens_r = n1[p]
+        # destination of local entry t of local pair x: goffs[p[x]] + t
+        starts = np.repeat(goffs[p] - np.concatenate([[0], np.cumsum(lens_r)[:-1]]), lens_r)
+        out_m[starts + np.arange(int(lens_r.sum()))] = a[2 * k: 2 * k + int(lens_r.sum())]
     return out_c, out_m, goffs
 
 
