@@ -91,3 +91,44 @@ def test_two_rank_gather_and_nccl_id():
     assert res[0] == ref_c.tolist()
     assert res[1] == [m.tolist() for m in ref_m]
     assert got[1][0] is None
+
+
+def _gather_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_00830_b200 import dist as fdist
+        npairs = 13
+        n1 = [(k * 7) % 5 for k in range(npairs)]  # unequal mapping lengths, some empty
+        idx = fdist.shard_pairs(npairs, rank, world)
+        costs = np.array([(1 << 40) + 3 * int(k) for k in idx], np.int64)  # costs beyond 2^31
+        maps = [np.arange(n1[int(k)], dtype=np.int32) + 100 * int(k) for k in idx]
+        offs = np.concatenate([[0], np.cumsum([m.shape[0] for m in maps])]).astype(np.int64)
+        flat = np.concatenate(maps + [np.zeros(0, np.int32)]).astype(np.int32)
+        res = fdist.gather_results(npairs, idx, costs, flat, offs, n1)
+        q.put((rank, None if res is None else (res[0].tolist(), res[1].tolist(), res[2].tolist())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_three_rank_gather_unequal_lengths():
+    """gather_results with 3 ranks: unequal per-rank lengths (padding), empty mappings, int64 costs > 2^31."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[1] is None and got[2] is None
+    c, m, o = got[0]
+    n1 = [(k * 7) % 5 for k in range(13)]
+    assert c == [(1 << 40) + 3 * k for k in range(13)]
+    assert o == [0] + list(np.cumsum(n1))
+    assert m == [100 * k + t for k in range(13) for t in range(n1[k])]
