@@ -1002,7 +1002,7 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     size_t static_smem = 0;
     {
         cudaFuncAttributes fa;
-        CK(cudaFuncGetAttributes(&fa, (const void *)fg::kbest_large_kernel<uint16_t, uint16_t, true, true>));
+        CK(cudaFuncGetAttributes(&fa, (const void *)fg::kbest_large_kernel<uint16_t, uint16_t, true, 2>));
         static_smem = fa.sharedSizeBytes;
     }
     const size_t smem_cap = (size_t)h->smem_optin - static_smem;
@@ -1017,7 +1017,8 @@ void solve_large(fastged_handle_t *h, const fastged_graph_t *g1, const fastged_g
     const size_t smem = fg::large_smem_bytes(cs, csz, n1s, esz, nwa, n1r, W, n2, nnbr, adjT_in_smem, csr_in_smem);
     if (smem > smem_cap) fail(FASTGED_ERR_CAPACITY, "large-mode kernel needs %zu B of shared memory", smem);
     void *kfn = nullptr;
-#define LK(M, C, L) (sharded ? (void *)fg::kbest_large_kernel<M, C, L, true> : (void *)fg::kbest_large_kernel<M, C, L, false>)
+#define LK(M, C, L) (virt ? (void *)fg::kbest_large_kernel<M, C, L, 2> \
+                         : real ? (void *)fg::kbest_large_kernel<M, C, L, 1> : (void *)fg::kbest_large_kernel<M, C, L, 0>)
     if (wide) kfn = c16 ? (lab ? LK(uint16_t, uint16_t, true) : LK(uint16_t, uint16_t, false))
                         : (lab ? LK(uint16_t, uint8_t, true) : LK(uint16_t, uint8_t, false));
     else kfn = c16 ? (lab ? LK(uint8_t, uint16_t, true) : LK(uint8_t, uint16_t, false))

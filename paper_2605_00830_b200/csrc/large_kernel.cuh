@@ -232,9 +232,11 @@ __device__ unsigned int fg_dbg_bad;
 #ifdef FG_LSTAT
 __device__ unsigned long long fg_lstat[2];
 #endif
-// SHARD = false: one GPU (G = 1); every sharding quantity folds to a constant, so the single-GPU
-// kernel carries no register cost for the sharded mode.
-template <typename MapT, typename CntT, bool LAB, bool SHARD>
+// SHARD = 0: one GPU (G = 1); every sharding quantity folds to a constant, so the single-GPU kernel carries
+// no register cost for the sharded mode.  SHARD = 1: one rank per GPU (the rank from the parameters, the own
+// arrays at fixed addresses).  SHARD = 2: virtual ranks = CTA groups of this grid (rank, CTA index and the
+// own arrays' offset from shared memory).
+template <typename MapT, typename CntT, bool LAB, int SHARD>
 __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) {
     extern __shared__ __align__(16) uint8_t dsmem[];
     constexpr int NWB = LNT / 32;
@@ -267,9 +269,9 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         for (int x = threadIdx.x; x < G * (int)(sizeof(LargeArgs::Rank) / 8); x += LNT)
             reinterpret_cast<unsigned long long *>(s_rk)[x] = reinterpret_cast<const unsigned long long *>(a.rk)[x];
     block_sync();
-#define RANK (SHARD ? s_rank : 0)
-#define LB (SHARD ? s_lb : (int)blockIdx.x)
-#define ML(f) (SHARD ? fg_loc(a.self.f, s_roff) : a.self.f)
+#define RANK (SHARD == 2 ? s_rank : (SHARD == 1 ? a.rank : 0))
+#define LB (SHARD == 2 ? s_lb : (int)blockIdx.x)
+#define ML(f) (SHARD == 2 ? fg_loc(a.self.f, s_roff) : a.self.f)
     // field f of rank r's arrays (a peer's memory when sharded)
 #define RK(r, f) (SHARD ? s_rk[r].f : a.self.f)
     // the one CTA that writes the home-only outputs
@@ -285,10 +287,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     // the remote descriptor writes and home atomics of every CTA are visible past it)
     // Returns false (on every CTA of the rank) when a peer did not arrive within xtimeout_ns.
     auto xsync = [&]() -> bool {
-        if (SHARD && G > 1 && !a.virt) __threadfence_system();
+        if (SHARD == 1 && G > 1) __threadfence_system();
         block_sync();
         grid.sync();
-        if (SHARD && G > 1 && !a.virt) {
+        if (SHARD == 1 && G > 1) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 const unsigned xepoch = (s_xepoch += (unsigned)G);
                 atomicAdd_system(a.bar, 1u);

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_00830_b200 import binding, synth, build
 build.build()
 w = synth.config_workload(4)
-for idx in (0, 4):
+for idx in (0, 4, 5):
     g1, g2 = w.pair(idx)
     K = w.run_K[idx]
     h = binding.Handle(0)
