@@ -46,9 +46,6 @@
 namespace fg {
 namespace cg = cooperative_groups;
 
-#ifndef FG_LBR
-#define FG_LBR 4 // rows of one B-phase step with their code loads in flight together
-#endif
 #ifndef FG_LNT
 #define FG_LNT 640
 #endif
