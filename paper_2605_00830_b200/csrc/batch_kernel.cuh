@@ -40,7 +40,7 @@
 namespace fg {
 
 #ifndef FG_CZ
-#define FG_CZ 4 // children evaluated per iteration of the wide branch loop (independent chains)
+#define FG_CZ 2 // children evaluated per iteration of the wide branch loop (independent chains; 2 measured best: 49.6 vs 50.8 ms at 4)
 #endif
 #ifndef FG_MINBLOCKS
 #define FG_MINBLOCKS 2 // resident CTAs per SM requested from ptxas (A/B experiments)
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? FG_MINBLOCKS_128 : FG_MINBLOCK
                                 return min(max(x, 0), win + 1);
                             };
                             uint32_t F = Vm[w] & ~U[w];
-                            while (F) { // four free targets per iteration (independent chains); lb = 0: no child
+                            while (F) { // FG_CZ free targets per iteration (independent chains); lb = 0: no child
                                 uint32_t lz[FG_CZ];
 #pragma unroll
                                 for (int z = 0; z < FG_CZ; ++z) { lz[z] = F & (0u - F); F ^= lz[z]; }
