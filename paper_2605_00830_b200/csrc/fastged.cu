@@ -535,8 +535,14 @@ constexpr int BATCH_NT = FG_BATCH_NT; // threads per CTA of the batched kernel (
 #ifndef FG_BATCH_NT_W1
 #define FG_BATCH_NT_W1 128
 #endif
-// one-word pairs (n2 <= 32) have small work arrays: a narrower CTA puts more pairs on an SM
+#ifndef FG_BATCH_NT_W1_LAB
+#define FG_BATCH_NT_W1_LAB 256
+#endif
+// one-word pairs (n2 <= 32) have small work arrays: a narrower CTA puts more pairs on an SM (unlabelled:
+// 128 threads measured best); labelled one-word pairs, whose update builds the label planes, run faster at
+// 256 threads (cfg5 slice 103.0 -> 100.1 ms; unlabelled cfg3 49.5 -> 50.1 ms, so not for those)
 constexpr int BATCH_NT_W1 = FG_BATCH_NT_W1;
+constexpr int BATCH_NT_W1_LAB = FG_BATCH_NT_W1_LAB;
 
 constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batches into two pipelined chunks
 
@@ -544,16 +550,16 @@ constexpr int32_t PIPELINE_MIN_PAIRS = 4096; // solve_batch splits larger batche
 // has at most SMALL_CHILDREN candidates (e.g. AIDS-like pairs at K = 100: up to 16 pairs in flight per SM
 // instead of 2, no cross-warp barriers), 128 for the other one-word groups, 256 otherwise.
 constexpr int64_t SMALL_CHILDREN = 4096;
-int batch_nt(int W, int64_t kcap, int n2max) {
+int batch_nt(int W, bool lab, int64_t kcap, int n2max) {
     if (W == 1 && kcap * (n2max + 1) <= SMALL_CHILDREN) return 32;
-    return W == 1 ? BATCH_NT_W1 : BATCH_NT;
+    return W == 1 ? (lab ? BATCH_NT_W1_LAB : BATCH_NT_W1) : BATCH_NT;
 }
 
 void *batch_kernel_for(int W, bool lab, bool smem, int nt) {
 #define KV(WW, LL, SS, NN) \
     if (W == WW && lab == LL && smem == SS && nt == NN) return (void *)fg::kbest_batch_kernel<WW, LL, NN, SS>;
     KV(1, false, true, 32) KV(1, true, true, 32)
-    KV(1, false, true, BATCH_NT_W1) KV(1, true, true, BATCH_NT_W1) KV(1, false, false, BATCH_NT_W1) KV(1, true, false, BATCH_NT_W1)
+    KV(1, false, true, BATCH_NT_W1) KV(1, false, false, BATCH_NT_W1) KV(1, true, true, BATCH_NT_W1_LAB) KV(1, true, false, BATCH_NT_W1_LAB)
     KV(2, false, true, BATCH_NT) KV(2, true, true, BATCH_NT) KV(3, false, true, BATCH_NT) KV(3, true, true, BATCH_NT)
     KV(4, false, true, BATCH_NT) KV(4, true, true, BATCH_NT)
     KV(2, false, false, BATCH_NT) KV(2, true, false, BATCH_NT)
@@ -708,7 +714,7 @@ void run_batch(fastged_handle_t *h, fastged_batch *b, const fastged_costs_t *c, 
         a.sm.bytes = (int)smem;
         size_t per_cta = 2 * Kc * (4 + 4 * (size_t)W + 4 * (size_t)W * NB + (size_t)a.n1max) + (in_smem ? 0 : wk);
         per_cta = (per_cta + 255) & ~(size_t)255;
-        const int nt = in_smem ? batch_nt(W, kcap, n2max) : batch_nt(W, 1 << 30, n2max);
+        const int nt = in_smem ? batch_nt(W, key.lab, kcap, n2max) : batch_nt(W, key.lab, 1 << 30, n2max);
         void *kern = batch_kernel_for(W, key.lab, in_smem, nt);
         if (!kern) fail(FASTGED_ERR_ARG, "no kernel variant for W=%d", W);
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
