@@ -47,7 +47,7 @@ namespace fg {
 namespace cg = cooperative_groups;
 
 #ifndef FG_LNT
-#define FG_LNT 640
+#define FG_LNT 736
 #endif
 constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per SM)
 #ifndef FG_C1_LIGHT
