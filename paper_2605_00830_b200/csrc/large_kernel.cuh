@@ -401,7 +401,10 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             }
         const int edd = c.edel * d, ee = c.edel + c.eins, pedDel = c.vdel + edd;
         // cB by scatter over neighbour lists, or by popcount over the nonzero words of B_p (uniform choice)
-        const bool scatter = LAB || (d * a.degw * 8 < S * min(W, d) * 13);
+#ifndef FG_SCATTER_RATIO
+#define FG_SCATTER_RATIO 13 // scatter when d * ceil(deg / 32) * 8 < S * min(W, d) * FG_SCATTER_RATIO
+#endif
+        const bool scatter = LAB || (d * a.degw * 8 < S * min(W, d) * FG_SCATTER_RATIO);
         const int chunk = (Nl + GW - 1) / GW; // B / C1: static contiguous code ranges per warp (local rows)
         const int p0 = min(Nl, gw * chunk), p1 = min(Nl, p0 + chunk);
         const int cchunk = (Nl + nb - 1) / nb; // A: this CTA's parents, taken dynamically
