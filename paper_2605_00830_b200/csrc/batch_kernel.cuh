@@ -133,6 +133,15 @@ __device__ __forceinline__ void block_sync() {
 #endif
 }
 
+// The same barrier as the aligned bar.sync: the volatile bar.warp.sync reconverges the warp first, so
+// every warp arrives converged with no instruction between the two.  The whole-GPU kernel uses it
+// (FG_LARGE_ALIGNED_BARRIER, default on: n = 500 K = 1e5 136 -> 127 ms, its B / C1 phases -35 %);
+// the batched kernel measured no difference and keeps block_sync.
+__device__ __forceinline__ void block_sync_aligned() {
+    asm volatile("bar.warp.sync -1;" ::: "memory");
+    asm volatile("bar.sync 0;" ::: "memory");
+}
+
 // Position of the (r+1)-th set bit of x (0 <= r < popc(x)): popcount bisection, no data-dependent loop.
 __device__ __forceinline__ int select_bit(uint32_t x, int r) {
     int pos = 0, c;

@@ -50,6 +50,16 @@ namespace cg = cooperative_groups;
 #define FG_LNT 736
 #endif
 constexpr int LNT = FG_LNT; // threads per CTA of the large kernel (one CTA per SM)
+#ifndef FG_LARGE_ALIGNED_BARRIER
+#define FG_LARGE_ALIGNED_BARRIER 1
+#endif
+__device__ __forceinline__ void lsync() {
+#if FG_LARGE_ALIGNED_BARRIER
+    block_sync_aligned();
+#else
+    block_sync();
+#endif
+}
 #ifndef FG_C1_LIGHT
 #define FG_C1_LIGHT 8 // C1: rows with at most this many survivors are emitted lane per row
 #endif
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     if (SHARD)
         for (int x = threadIdx.x; x < G * (int)(sizeof(LargeArgs::Rank) / 8); x += LNT)
             reinterpret_cast<unsigned long long *>(s_rk)[x] = reinterpret_cast<const unsigned long long *>(a.rk)[x];
-    block_sync();
+    lsync();
 #define RANK (SHARD == 2 ? s_rank : (SHARD == 1 ? a.rank : 0))
 #define LB (SHARD == 2 ? s_lb : (int)blockIdx.x)
 #define ML(f) (SHARD == 2 ? fg_loc(a.self.f, s_roff) : a.self.f)
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
     // Returns false (on every CTA of the rank) when a peer did not arrive within xtimeout_ns.
     auto xsync = [&]() -> bool {
         if (SHARD == 1 && G > 1) __threadfence_system();
-        block_sync();
+        lsync();
         grid.sync();
         if (SHARD == 1 && G > 1) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                     __nanosleep(256);
                 }
             }
-            block_sync();
+            lsync();
             grid.sync();
             return *(volatile int32_t *)a.xerr == 0;
         }
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
         // term of its PED cancels: total = PED_p + comp_p - vins + cv + edel d - (edel + eins) cB (+ mis)
         const bool lastTot = a.last_by_total && i == n1 - 1;
         int tcode = 0, rq = 0;
-        block_sync(); // P_i staged
+        lsync(); // P_i staged
 
         for (;;) { // ---------------- A + T ----------------
             // Children with PED > U_i = max parent PED + vdel + edel d_i are never selected when N >= K
@@ -434,7 +444,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
             if (threadIdx.x == 0) { s_cnt = 0; s_next = cb0; s_drop = 0; }
             if (home0())
                 for (int k = threadIdx.x; k < 256; k += LNT) a.hist[((ps + 1) % 3) * 256 + k] = 0;
-            block_sync();
+            lsync();
             int wcount = 0;
             if (brancher) {
                 // 3-stage pipeline per warp: descriptor loads (registers) -> row prefetch (cp.async into the
@@ -675,7 +685,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 cpa_wait<0>();
             }
             if (first && lane == 0) atomicAdd((unsigned long long *)&s_cnt, (unsigned long long)wcount);
-            block_sync();
+            lsync();
             int *gh = a.hist + (ps % 3) * 256;
             for (int bin = threadIdx.x; bin < 256; bin += LNT) {
                 int v = 0;
@@ -726,11 +736,11 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                         s_pre[1] = incl; // every code of the window lies below the K-th smallest
                     }
                 }
-                block_sync();
+                lsync();
                 tcode = s_pre[0];
                 if (tcode) rq = s_pre[1];
                 else { retry = slide = true; below += s_pre[1]; }
-                block_sync();
+                lsync();
             }
             if (first) children += ci;
             ps++;
@@ -781,7 +791,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 we += __shfl_sync(FULL, ie, 31);
             }
             if (lane == 0) { s_red[0][wib] = wl; s_red[1][wib] = we; }
-            block_sync();
+            lsync();
             if (lane == 0) { // this warp's prefix inside the CTA
                 int cl = 0, ce = 0;
                 for (int w = 0; w < wib; ++w) { cl += s_red[0][w]; ce += s_red[1][w]; }
@@ -812,7 +822,7 @@ __global__ void __launch_bounds__(LNT, 1) kbest_large_kernel(const LargeArgs a) 
                 re += __shfl_sync(FULL, ie, 31);
             }
         }
-        block_sync();
+        lsync();
         const int Nn = keepall ? (int)a.ci[i] : K;
 
         // ---------------- C1: compact survivors in (parent, child) order, with their PEDs ----------------
